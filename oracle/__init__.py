@@ -1,0 +1,128 @@
+"""ctypes binding of the CPU oracle (oracle/sdtw_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / ``--impl reference`` legs of bench.py -- never by the product
+package ``paper_2403_06931_b200``. It shares no code with the CUDA path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sdtw_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-pthread"]
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (no FP contraction, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        f32p = ctypes.POINTER(ctypes.c_float)
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        i64 = ctypes.c_int64
+        L.oracle_sdtw.argtypes = [f32p, i64, i64, f32p, i64, ctypes.c_int, f32p, i64p, i64p, f32p, ctypes.c_int]
+        L.oracle_sdtw.restype = ctypes.c_int
+        L.oracle_sdtw_full.argtypes = [f32p, i64, f32p, i64, ctypes.c_int, f32p, i64p]
+        L.oracle_sdtw_full.restype = ctypes.c_int
+        L.oracle_walkback.argtypes = [f32p, i64, i64, i64]
+        L.oracle_walkback.restype = i64
+        L.oracle_znorm.argtypes = [f32p, i64, i64, f32p]
+        L.oracle_znorm.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _f32(a):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def _i64(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+def sdtw(Q, Y, fma: bool = True, start: bool = False, last_rows: bool = False,
+         threads: int | None = None):
+    """Batched sDTW on raw inputs (no normalisation). Q: [Z,N] or [N]; Y: [M].
+
+    Returns dict(cost[Z] f32, end[Z] i64, start[Z] i64 | None, last_rows[Z,M] | None)."""
+    Q = np.asarray(Q, dtype=np.float32)
+    if Q.ndim == 1:
+        Q = Q[None, :]
+    Z, N = Q.shape
+    Qc, qp = _f32(Q)
+    Yc, yp = _f32(Y)
+    M = Yc.shape[0]
+    cost = np.empty(Z, np.float32)
+    end = np.empty(Z, np.int64)
+    st = np.empty(Z, np.int64) if start else None
+    lr = np.empty((Z, M), np.float32) if last_rows else None
+    if threads is None:
+        threads = os.cpu_count() or 1
+    rc = lib().oracle_sdtw(qp, Z, N, yp, M, int(bool(fma)),
+                           cost.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), _i64(end),
+                           _i64(st) if st is not None else None,
+                           lr.ctypes.data_as(ctypes.POINTER(ctypes.c_float)) if lr is not None else None,
+                           int(threads))
+    if rc != 0:
+        raise ValueError("oracle_sdtw: bad arguments")
+    return dict(cost=cost, end=end, start=st, last_rows=lr)
+
+
+def sdtw_full(x, Y, fma: bool = True):
+    """Full D and S matrices (N x M) for one query -- small instances only."""
+    xc, xp = _f32(x)
+    Yc, yp = _f32(Y)
+    N, M = xc.shape[0], Yc.shape[0]
+    D = np.empty((N, M), np.float32)
+    S = np.empty((N, M), np.int64)
+    rc = lib().oracle_sdtw_full(xp, N, yp, M, int(bool(fma)),
+                                D.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), _i64(S))
+    if rc != 0:
+        raise ValueError("oracle_sdtw_full: bad arguments")
+    return D, S
+
+
+def walkback(D, end: int) -> int:
+    Dc, dp = _f32(D)
+    N, M = Dc.shape
+    return int(lib().oracle_walkback(dp, N, M, int(end)))
+
+
+def znorm(X):
+    """Per-series z-normalisation (Eq. 2), fp64 accumulation, fp32 out."""
+    X = np.asarray(X, dtype=np.float32)
+    shape = X.shape
+    if X.ndim == 1:
+        X = X[None, :]
+    Xc, xp = _f32(X)
+    out = np.empty_like(Xc)
+    rc = lib().oracle_znorm(xp, Xc.shape[0], Xc.shape[1],
+                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+    if rc != 0:
+        raise ValueError("oracle_znorm: bad arguments")
+    return out.reshape(shape)
+
+
+def sdtw_normalized(Q, Y, fma: bool = True, start: bool = False, threads: int | None = None):
+    """End-to-end oracle: z-normalise reference (globally) and each query, then sDTW
+    (§5: runSDTW normalises both the reference and the batch)."""
+    Yn = znorm(np.asarray(Y, np.float32)[None, :])[0]
+    Qn = znorm(Q)
+    return sdtw(Qn, Yn, fma=fma, start=start, threads=threads)
