@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""bench.py -- batched subsequence DTW (arXiv 2403.06931) on B200.
+
+Metric (BASELINE.json): GCUPS = cell updates / s = Z*N*M / t, whole job over all
+ranks.  One "step" = one pass of the whole hot path over one batch: query
+z-normalisation + wavefront DP + min/argmin epilogue (+ the one all-gather of
+per-query records when N>1), through the public API (sdtw_batch) on inputs
+already resident in HBM.  Default workload (`--config c3`): 512 x 2,000-sample
+queries per GPU against a 10M-sample synthetic nanopore-like reference
+(BASELINE configs 3 at 1 GPU; 4,096 queries at 8 GPUs = config 4), weak scaling.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c4|c5_500|...]
+                    [--impl ours|reference] [--scaling weak|strong]
+
+Timing: per step, L2 is flushed (a 256 MiB write, outside the timed window), then
+CUDA events on torch's current stream bracket the step; barrier + synchronize on
+both sides; rank 0 reports the max over ranks.  The DP kernel is also timed on
+its own stream by the library (SDTW_OPT_PROFILE) for the roofline object.
+`--impl reference` times the CPU oracle (oracle/) on a bounded sample of the
+same workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# ALU roofline: SMs x 128 FP32 lanes x f_SM / (SASS issue slots per cell)
+LANES_PER_SM = 128
+SASS_PER_CELL = {"packed_fma": 2.0, "scalar_fma": 3.0, "scalar_nofma": 4.0, "packed_nofma": 3.5,
+                 "packed_fma_trace": 6.0, "scalar_fma_trace": 7.0}
+
+
+def gsps(floats: float, ms: float) -> float:
+    """PAPER.md Eq. 3: floatsProcessed / (milliseconds * 1e9 / 1000)."""
+    if ms <= 0:
+        raise ValueError("ms must be > 0")
+    return floats / (ms * 1e9 / 1000.0)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for n, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "power_w_max": max(pw) if pw else None,
+                "samples": len(self.samples)}
+
+
+def _workload(cfg_name: str, rank: int, world: int, scaling: str):
+    from datagen import CONFIGS, nanopore_queries, nanopore_reference
+    cfg = dict(CONFIGS[cfg_name])
+    Z, N, M, seed = cfg["Z"], cfg["N"], cfg["M"], cfg["seed"]
+    if scaling == "weak":
+        Zl, first = Z, rank * Z
+        Zg = Z * world
+    else:
+        per = -(-Z // world)
+        first = rank * per
+        Zl = max(0, min(Z, first + per) - first)
+        Zg = Z
+    Y = nanopore_reference(M, seed)
+    Q = nanopore_queries(Zl, N, M, seed, first_query=first)
+    return Q, Y, dict(Z=Zg, Z_local=Zl, N=N, M=M, seed=seed, start=cfg["start"])
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, on a bounded sample, host cores."""
+    import oracle
+    from datagen import CONFIGS, nanopore_queries, nanopore_reference
+    cfg = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    N = cfg["N"]
+    # bounded sample: `threads` queries x N against the first Ms reference samples,
+    # sized for ~2-4 s per step at ~0.3 GCUPS per core
+    Ms = int(min(cfg["M"], max(2000, 1.0e9 / N)))
+    Y = nanopore_reference(cfg["M"], cfg["seed"])[:Ms]
+    Q = nanopore_queries(threads, N, cfg["M"], cfg["seed"])
+    Yn = oracle.znorm(Y[None])[0]
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        Qn = oracle.znorm(Q)
+        oracle.sdtw(Qn, Yn, fma=True, start=cfg["start"], threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    cells = float(threads) * N * Ms
+    tot = sum(times)
+    val = cells * len(times) / tot / 1e9
+    sample = "%d queries x %d samples (config %s inputs) vs the first %d reference samples, %d host threads" % (
+        threads, N, args.config, Ms, threads)
+    line = {
+        "impl": "reference", "metric": "GCUPS", "value": val, "unit": "GCUPS", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic nanopore-like (datagen), seeded",
+        "config": {"workload": args.config, "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "GCUPS", "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_leg(args, Q, Y, N):
+    """The oracle timed on the host cores, rank 0, N=1, bounded sample (~10-30 s)."""
+    import oracle
+    threads = os.cpu_count() or 1
+    Ms = int(min(Y.shape[0], max(2000, 2.0e9 / N)))
+    nq = min(Q.shape[0], threads)
+    Yn = oracle.znorm(Y[:Ms][None])[0]
+    Qn = oracle.znorm(Q[:nq])
+    t0 = time.perf_counter()
+    oracle.sdtw(Qn, Yn, fma=True, threads=threads)
+    dt = time.perf_counter() - t0
+    cells = float(nq) * N * Ms
+    return {"value": cells / dt / 1e9, "unit": "GCUPS", "cores": threads, "kind": "oracle",
+            "sample": "%d queries x %d vs first %d reference samples of the same inputs, %d threads, %.1f s"
+                      % (nq, N, Ms, threads, dt)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2403_06931_b200 as sd
+    from paper_2403_06931_b200.distributed import distributed_batch
+
+    Q, Y, w = _workload(args.config, rank, world, args.scaling)
+    N, M = w["N"], w["M"]
+    trace = bool(w["start"])
+    sd.set_reference(torch.from_numpy(Y).to(dev))
+    Qd = torch.from_numpy(Q).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if world > 1:
+            return distributed_batch(Qd, traceback=trace, pre_sharded=True, device=dev)
+        return sd.traceback(Qd) if trace else sd.batch(Qd)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    dp_ms = []
+    launches0 = sd.launch_count()
+    sampler = ClockSampler(local)
+    with sd.options(OPT_PROFILE=1), sampler:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            dp_ms.append(sd.profile()[0])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = sd.launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    cells_step = float(w["Z"]) * N * M
+    value = cells_step * args.steps / (tot_ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel (the DP kernel), measured on its own stream
+    peaks, src = _peaks()
+    fmax = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    packed = sd.get_option(sd.OPT_PACKED) != 0
+    mix = ("packed" if packed else "scalar") + "_fma" + ("_trace" if trace else "")
+    k = SASS_PER_CELL[mix]
+    peak = sms * LANES_PER_SM * fmax * 1e6 / k / 1e9
+    peak3 = sms * LANES_PER_SM * fmax * 1e6 / 3.0 / 1e9
+    dp_avg = statistics.mean(dp_ms)
+    achieved = float(w["Z_local"]) * N * M / (dp_avg / 1e3) / 1e9
+    clocks = sampler.summary()
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "GCUPS", "frac": achieved / peak,
+            "traffic": None, "sass_per_cell": k, "peak_source": "%s sm_max_mhz=%.0f x %d SMs x %d lanes / %g"
+            % (src, fmax, sms, LANES_PER_SM, k),
+            "headline_peak_k3": peak3, "headline_frac_k3": achieved / peak3,
+            "dp_kernel_ms": dp_avg}
+    if clocks.get("sm_mhz"):
+        roof["frac_at_sampled_clock"] = achieved / (peak * clocks["sm_mhz"] / fmax)
+
+    # e2e: the same metric through the public API with host buffers (pinned), copies inside
+    e2e = None
+    if not args.no_e2e:
+        Qh = torch.from_numpy(Q).pin_memory()
+        sd.batch(Qh.numpy()) if not trace else sd.traceback(Qh.numpy())
+        ts = []
+        for i in range(max(1, min(args.steps, 3))):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            if world > 1:
+                distributed_batch(Qh.numpy(), traceback=trace, pre_sharded=True, device=dev)
+            else:
+                (sd.traceback if trace else sd.batch)(Qh.numpy())
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        te = sum(ts)
+        if world > 1:
+            t = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": cells_step * len(ts) / te / 1e9, "unit": "GCUPS",
+               "h2d_bytes_per_step": int(Q.nbytes) * world,
+               "d2h_bytes_per_step": int(w["Z"]) * (4 + 8 + (8 if trace else 0))}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_leg(args, Q, Y, N)
+
+    if rank == 0:
+        line = {
+            "metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic nanopore-like signals (datagen, seeded); random reference, no trained weights",
+            "config": {"workload": "%s: %d x %d queries vs %d-sample reference%s" % (
+                args.config, w["Z"], N, M, " (start index on)" if trace else ""),
+                "queries_per_gpu": w["Z_local"], "N": N, "M": M, "normalize": True, "fma": True,
+                "packed": packed, "l2": "flushed (256 MiB write) before every timed step",
+                "parallelism": "query-sharded x%d, reference replicated" % world},
+            "gpu_launches": launches, "roofline": roof, "clocks": clocks,
+            "gsps_eq3": gsps(float(w["Z"]) * N, tot_ms / args.steps),
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -79,13 +79,16 @@ def nanopore_reference(M: int, seed: int) -> np.ndarray:
 
 
 def nanopore_queries(Z: int, N: int, M: int, seed: int,
-                     on_target: float = 0.5) -> np.ndarray:
-    """Z x N raw (pA-like) queries, row-major, contiguous (§5.1)."""
+                     on_target: float = 0.5, first_query: int = 0) -> np.ndarray:
+    """Z x N raw (pA-like) queries, row-major, contiguous (§5.1).
+
+    Queries first_query .. first_query+Z-1 of the stream for (seed, M): a rank of a
+    sharded job generates only its own shard."""
     levels = _levels(seed)
     ref_genome = _ref_genome(seed, M)
     out = np.empty((Z, N), dtype=np.float32)
     for q in range(Z):
-        rng = _rng(seed, 1000 + q)
+        rng = _rng(seed, 1000 + first_query + q)
         n_bases = max(8, N // 9 + 16)
         while True:
             if rng.random() < on_target and M >= n_bases + _K:

@@ -1,0 +1,109 @@
+/*
+ * sdtw.h -- C ABI of the B200-native batched subsequence-DTW engine
+ * (arXiv 2403.06931, "sDTW on AMD GPUs with HIP/ROCm"; citations P:Lnn are
+ * lines of that paper's PAPER.md, S:Lnn of SPEC.md).
+ *
+ * Problem (§2, Eq. 1): for every query X (length N) of a
+ * batch, fill the N x M matrix
+ *     D(i,j) = min{D(i-1,j), D(i,j-1), D(i-1,j-1)} + (X_i - Y_j)^2
+ * against one long reference Y (length M), with a free start anywhere in row 0
+ * (virtual row -1 = 0, virtual column -1 = +inf), and report
+ *     cost = min_j D(N-1,j),  end = smallest j attaining it,
+ * and optionally the start column of that warp path (P:L35 walk-back).
+ * Everything is fp32; see DESIGN.md §2 for every reading of the paper.
+ *
+ * Threading / devices: one library context per CUDA device; every call acts on
+ * the CURRENT device (cudaGetDevice).  A multi-GPU job runs one process per
+ * GPU and calls the ABI once per rank.  Calls are not re-entrant on one device.
+ *
+ * Pointers: Q / in / out / Y may be host or device pointers (detected with
+ * cudaPointerGetAttributes; device pointers must live on the current device).
+ * The caller owns them.  All calls are synchronous: they return after the
+ * results are written (work is enqueued on the SDTW_OPT_STREAM stream, then
+ * that stream is synchronised).  No partial results are written on error.
+ */
+#ifndef SDTW_H
+#define SDTW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SDTW_OK = 0,
+    SDTW_E_ARG = 1,        /* N<1, M<1, n<0, NULL pointer with n>0, bad option */
+    SDTW_E_NOREF = 2,      /* sdtw_batch/traceback before sdtw_set_reference */
+    SDTW_E_CUDA = 3,       /* CUDA runtime error (text in sdtw_last_error) */
+    SDTW_E_NOMEM = 4,      /* device allocation failed */
+    SDTW_E_NONFINITE = 5   /* an input sample is NaN or +-inf */
+} sdtw_status;
+
+/* Option keys for sdtw_set_option / sdtw_get_option (process-wide). */
+enum {
+    SDTW_OPT_NORMALIZE = 1, /* 1 (default): z-normalise reference (at set_reference) and
+                               each query (§5.1 Eq. 2, "normalize both");
+                               0: raw samples */
+    SDTW_OPT_FMA = 2,       /* 1 (default): cell = fmaf(t,t,m); 0: fl(fl(t*t)+m) -- both
+                               bit-exact with the oracle in the same mode */
+    SDTW_OPT_SEGMENT_W = 3, /* reference columns per lane ("segment width");
+                               0 = auto */
+    SDTW_OPT_LANES = 4,     /* warps per CTA in one query ring; 0 = auto */
+    SDTW_OPT_CLUSTER = 5,   /* CTAs per query (thread-block cluster, DSMEM handoff); 0 = auto */
+    SDTW_OPT_STREAM = 6,    /* cudaStream_t as int64 (0 = legacy default stream) */
+    SDTW_OPT_PACKED = 7,    /* 1: two chains per lane with f32x2 FADD2/FFMA2; 0: scalar;
+                               -1 (default) = auto */
+    SDTW_OPT_CHUNK = 8,     /* steps between inter-warp handoff checks (8,16,32); 0 = auto */
+    SDTW_OPT_PROFILE = 9    /* 1: time the DP kernel with CUDA events (sdtw_profile) */
+};
+
+/* Install the reference Y[M] on the current device (copied into a
+ * library-owned, +inf-padded buffer; z-normalised globally when
+ * SDTW_OPT_NORMALIZE=1).  Replaces any previous reference.  The caller may free
+ * Y on return.  Errors: SDTW_E_ARG (M<1, Y NULL), SDTW_E_NONFINITE, SDTW_E_NOMEM,
+ * SDTW_E_CUDA. */
+sdtw_status sdtw_set_reference(const float* Y, int64_t M);
+
+/* Batched sDTW.  Q: n_queries x N fp32, row-major, queries contiguous with no
+ * gaps.  out_cost[n_queries] fp32, out_end[n_queries] int64 (0-based
+ * smallest argmin column of the last row).  n_queries == 0 is a no-op.
+ * Errors: SDTW_E_ARG, SDTW_E_NOREF, SDTW_E_NONFINITE, SDTW_E_NOMEM, SDTW_E_CUDA. */
+sdtw_status sdtw_batch(const float* Q, int64_t n_queries, int64_t N,
+                       float* out_cost, int64_t* out_end);
+
+/* As sdtw_batch, plus out_start[n_queries] int64: the row-0 column where the
+ * optimal warp path of out_end begins (P:L35 walk-back; ties diag > up > left,
+ * DESIGN.md reading G6). */
+sdtw_status sdtw_traceback(const float* Q, int64_t n_queries, int64_t N,
+                           float* out_cost, int64_t* out_end, int64_t* out_start);
+
+/* z-normalisation of n_series contiguous series of length len (the paper's
+ * runNormalizer; Eq. 2 P:L73 with the population variance of P:L85-L86):
+ * fp64 accumulation, z = fl32((x - mean)/sd); degenerate series (var <= 1e-12 *
+ * E[x^2]) map to zeros.  in/out: n_series x len fp32 (may alias). */
+sdtw_status sdtw_znormalize(const float* in, int64_t n_series, int64_t len, float* out);
+
+sdtw_status sdtw_set_option(int key, int64_t value);
+sdtw_status sdtw_get_option(int key, int64_t* value);
+
+/* DP-kernel timing of the last sdtw_batch/traceback call when SDTW_OPT_PROFILE=1:
+ * *dp_ms = summed CUDA-event duration of the DP kernel launch(es) on the option
+ * stream; *launches = kernels the last call launched (all of them). */
+sdtw_status sdtw_profile(double* dp_ms, int64_t* launches);
+
+/* Total kernels this process has launched through the library. */
+int64_t sdtw_launch_count(void);
+
+/* Thread-local text describing the last non-OK status. */
+const char* sdtw_last_error(void);
+
+/* Free the current device's context (reference, workspaces). */
+void sdtw_release(void);
+
+int sdtw_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDTW_H */

@@ -1,0 +1,214 @@
+"""B200-native batched subsequence DTW (arXiv 2403.06931) -- Python binding.
+
+Argument marshalling only: every step of the hot path (z-normalisation, the
+wavefront DP, the min/argmin epilogue) runs in the sm_100a kernels of
+``libsdtw.so`` behind the C ABI of ``include/sdtw.h``.  There is no CPU
+fallback: importing this package fails loudly when the library is missing, and
+every call raises when the CUDA path fails.
+
+Functions mirror the ABI names (minus the ``sdtw_`` prefix):
+``set_reference``, ``batch``, ``traceback``, ``znormalize``, ``set_option``,
+``get_option``, ``profile``, ``launch_count``, ``release``.
+Inputs may be torch tensors (CUDA or CPU) or numpy arrays.  torch supplies
+device memory and the current stream (passed as SDTW_OPT_STREAM).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsdtw.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        "paper_2403_06931_b200: CUDA library %s is missing -- run "
+        "`python -m paper_2403_06931_b200.build` (or __graft_entry__.build()); "
+        "there is no CPU fallback" % LIB_PATH)
+
+_lib = ctypes.CDLL(LIB_PATH)
+_f32p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_lib.sdtw_set_reference.argtypes = [ctypes.c_void_p, _i64]
+_lib.sdtw_batch.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p]
+_lib.sdtw_traceback.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+_lib.sdtw_znormalize.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p]
+_lib.sdtw_set_option.argtypes = [ctypes.c_int, _i64]
+_lib.sdtw_get_option.argtypes = [ctypes.c_int, ctypes.POINTER(_i64)]
+_lib.sdtw_profile.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]
+_lib.sdtw_launch_count.restype = _i64
+_lib.sdtw_last_error.restype = ctypes.c_char_p
+_lib.sdtw_version.restype = ctypes.c_int
+for _n in ("sdtw_set_reference", "sdtw_batch", "sdtw_traceback", "sdtw_znormalize",
+           "sdtw_set_option", "sdtw_get_option", "sdtw_profile"):
+    getattr(_lib, _n).restype = ctypes.c_int
+
+# ABI constants (include/sdtw.h)
+OK, E_ARG, E_NOREF, E_CUDA, E_NOMEM, E_NONFINITE = range(6)
+OPT_NORMALIZE, OPT_FMA, OPT_SEGMENT_W, OPT_LANES, OPT_CLUSTER, OPT_STREAM, OPT_PACKED, OPT_CHUNK, \
+    OPT_PROFILE = range(1, 10)
+_STATUS = {0: "SDTW_OK", 1: "SDTW_E_ARG", 2: "SDTW_E_NOREF", 3: "SDTW_E_CUDA", 4: "SDTW_E_NOMEM",
+           5: "SDTW_E_NONFINITE"}
+
+EXPORTED_SYMBOLS = ("sdtw_set_reference", "sdtw_batch", "sdtw_traceback", "sdtw_znormalize",
+                    "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_launch_count",
+                    "sdtw_last_error", "sdtw_release", "sdtw_version")
+
+
+class SdtwError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("%s: %s" % (_STATUS.get(status, status), msg))
+        self.status = status
+
+
+def _check(rc: int):
+    if rc != OK:
+        raise SdtwError(rc, _lib.sdtw_last_error().decode(errors="replace"))
+
+
+def _torch():
+    try:
+        import torch
+        return torch
+    except ImportError:  # pragma: no cover
+        return None
+
+
+def _bind_stream(t):
+    """Route the library onto torch's current stream of the tensor's device."""
+    torch = _torch()
+    if torch is not None and isinstance(t, torch.Tensor) and t.is_cuda:
+        _check(_lib.sdtw_set_option(OPT_STREAM, torch.cuda.current_stream(t.device).cuda_stream))
+    else:
+        _check(_lib.sdtw_set_option(OPT_STREAM, 0))
+
+
+def _as_f32(x):
+    """(keepalive, pointer, shape) for a torch tensor or array-like, contiguous fp32."""
+    torch = _torch()
+    if torch is not None and isinstance(x, torch.Tensor):
+        t = x.detach()
+        if t.dtype != torch.float32:
+            t = t.float()
+        t = t.contiguous()
+        return t, t.data_ptr(), tuple(t.shape)
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    return a, a.ctypes.data, a.shape
+
+
+def version() -> int:
+    return int(_lib.sdtw_version())
+
+
+def set_option(key: int, value: int):
+    _check(_lib.sdtw_set_option(int(key), int(value)))
+
+
+def get_option(key: int) -> int:
+    v = _i64()
+    _check(_lib.sdtw_get_option(int(key), ctypes.byref(v)))
+    return int(v.value)
+
+
+def set_reference(Y):
+    """sdtw_set_reference(Y, M): install the reference on the current device."""
+    keep, ptr, shape = _as_f32(Y)
+    if len(shape) != 1:
+        raise ValueError("reference must be 1-D")
+    _bind_stream(keep)
+    _check(_lib.sdtw_set_reference(ctypes.c_void_p(ptr), shape[0]))
+
+
+def _outputs(keep, Z, trace):
+    torch = _torch()
+    if torch is not None and isinstance(keep, torch.Tensor) and keep.is_cuda:
+        dev = keep.device
+        cost = torch.empty(Z, dtype=torch.float32, device=dev)
+        end = torch.empty(Z, dtype=torch.int64, device=dev)
+        start = torch.empty(Z, dtype=torch.int64, device=dev) if trace else None
+        ptrs = (cost.data_ptr(), end.data_ptr(), start.data_ptr() if trace else 0)
+    else:
+        cost = np.empty(Z, np.float32)
+        end = np.empty(Z, np.int64)
+        start = np.empty(Z, np.int64) if trace else None
+        ptrs = (cost.ctypes.data, end.ctypes.data, start.ctypes.data if trace else 0)
+    return cost, end, start, ptrs
+
+
+def batch(Q):
+    """sdtw_batch: Q [Z, N] -> (cost[Z] fp32, end[Z] int64) on Q's device (numpy if host)."""
+    keep, ptr, shape = _as_f32(Q)
+    if len(shape) == 1:
+        shape = (1, shape[0])
+    Z, N = shape
+    cost, end, _, (pc, pe, _) = _outputs(keep, Z, False)
+    _bind_stream(keep)
+    _check(_lib.sdtw_batch(ctypes.c_void_p(ptr), Z, N, ctypes.c_void_p(pc), ctypes.c_void_p(pe)))
+    return cost, end
+
+
+def traceback(Q):
+    """sdtw_traceback: Q [Z, N] -> (cost, end, start)."""
+    keep, ptr, shape = _as_f32(Q)
+    if len(shape) == 1:
+        shape = (1, shape[0])
+    Z, N = shape
+    cost, end, start, (pc, pe, ps) = _outputs(keep, Z, True)
+    _bind_stream(keep)
+    _check(_lib.sdtw_traceback(ctypes.c_void_p(ptr), Z, N, ctypes.c_void_p(pc), ctypes.c_void_p(pe),
+                               ctypes.c_void_p(ps)))
+    return cost, end, start
+
+
+def znormalize(X):
+    """sdtw_znormalize (the paper's runNormalizer): per-series z-normalisation on the GPU."""
+    keep, ptr, shape = _as_f32(X)
+    rows = 1 if len(shape) == 1 else shape[0]
+    L = shape[-1]
+    torch = _torch()
+    if torch is not None and isinstance(keep, torch.Tensor) and keep.is_cuda:
+        out = torch.empty_like(keep)
+        po = out.data_ptr()
+    else:
+        out = np.empty(shape, np.float32)
+        po = out.ctypes.data
+    _bind_stream(keep)
+    _check(_lib.sdtw_znormalize(ctypes.c_void_p(ptr), rows, L, ctypes.c_void_p(po)))
+    return out
+
+
+def profile():
+    """(dp_ms, launches) of the last batch/traceback call (dp_ms needs OPT_PROFILE=1)."""
+    ms = ctypes.c_double()
+    n = _i64()
+    _check(_lib.sdtw_profile(ctypes.byref(ms), ctypes.byref(n)))
+    return float(ms.value), int(n.value)
+
+
+def launch_count() -> int:
+    return int(_lib.sdtw_launch_count())
+
+
+def release():
+    _lib.sdtw_release()
+
+
+class options:
+    """Context manager: temporarily set ABI options, e.g. ``with options(OPT_FMA=0): ...``."""
+
+    def __init__(self, **kw):
+        self.kw = {globals()[k] if isinstance(k, str) else k: v for k, v in kw.items()}
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            set_option(k, v)
+        return False

@@ -1,0 +1,466 @@
+// sdtw_api.cu -- host side of the C ABI declared in include/sdtw.h.
+//
+// Per-device context (reference buffer, workspaces, flags), option handling,
+// pointer-kind detection, launch-configuration choice and kernel dispatch.
+// Every step of the hot path runs in the kernels of sdtw_prep.cuh / sdtw_dp.cuh;
+// there is no CPU fallback: without a CUDA device every call returns SDTW_E_CUDA.
+#include "../../include/sdtw.h"
+#include "sdtw_dp.cuh"
+#include "sdtw_prep.cuh"
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Options {
+    int normalize = 1;
+    int fma = 1;
+    int segment_w = 0;
+    int lanes = 0;      // warps per CTA
+    int cluster = 0;
+    int packed = -1;
+    int chunk = 0;
+    int profile = 0;
+    cudaStream_t stream = 0;
+};
+Options g_opt;
+std::mutex g_mu;
+std::atomic<int64_t> g_launches{0};
+
+struct Ctx {
+    bool init = false;
+    int sms = 0;
+    float* ref = nullptr;
+    int64_t M = 0, Malloc = 0;
+    int ref_normalized = 0;
+    float* ws_q = nullptr;   size_t ws_q_n = 0;     // staged host queries
+    float* ws_x = nullptr;   size_t ws_x_n = 0;     // normalised queries
+    unsigned char* ws_out = nullptr; size_t ws_out_n = 0;
+    double* ws_part = nullptr;                      // reference partial sums + stats
+    int* flag_d = nullptr;
+    int* flag_h = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_dp_ms = 0.0;
+    int64_t last_launches = 0;
+};
+constexpr int kMaxDev = 64;
+Ctx g_ctx[kMaxDev];
+
+sdtw_status fail(sdtw_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+sdtw_status cuda_fail(cudaError_t e, const char* where) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? SDTW_E_NOMEM : SDTW_E_CUDA,
+                std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CK(call)                                          \
+    do {                                                  \
+        cudaError_t _e = (call);                          \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+sdtw_status get_ctx(Ctx** out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev < 0 || dev >= kMaxDev) return fail(SDTW_E_CUDA, "device index out of range");
+    Ctx& c = g_ctx[dev];
+    if (!c.init) {
+        CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaMalloc(&c.flag_d, 16));
+        CK(cudaHostAlloc(&c.flag_h, 16, cudaHostAllocDefault));
+        CK(cudaMalloc(&c.ws_part, sizeof(double) * (2 * 4096 + 8)));
+        CK(cudaEventCreate(&c.ev0));
+        CK(cudaEventCreate(&c.ev1));
+        c.init = true;
+    }
+    *out = &c;
+    return SDTW_OK;
+}
+
+template <class T>
+sdtw_status grow(T** p, size_t* have, size_t need_elems) {
+    if (*have >= need_elems) return SDTW_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    cudaError_t e = cudaMalloc(p, need_elems * sizeof(T));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(workspace)");
+    *have = need_elems;
+    return SDTW_OK;
+}
+
+// 1 = device pointer on the current device, 0 = host pointer, -1 = device pointer elsewhere
+int ptr_kind(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        return a.device == dev ? 1 : -1;
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------------ DP dispatch
+using sdtw::DpParams;
+typedef void (*DpKernel)(DpParams);
+
+template <int C, int WC>
+DpKernel pick_fma_trace(bool fma, bool trace) {
+    if (fma) return trace ? sdtw::sdtw_dp_kernel<C, WC, true, true> : sdtw::sdtw_dp_kernel<C, WC, true, false>;
+    return trace ? sdtw::sdtw_dp_kernel<C, WC, false, true> : sdtw::sdtw_dp_kernel<C, WC, false, false>;
+}
+
+DpKernel pick_kernel(int C, int WC, bool fma, bool trace) {
+    if (C == 1) {
+        switch (WC) {
+            case 8: return pick_fma_trace<1, 8>(fma, trace);
+            case 16: return pick_fma_trace<1, 16>(fma, trace);
+            case 32: return pick_fma_trace<1, 32>(fma, trace);
+            default: return nullptr;
+        }
+    }
+    switch (WC) {
+        case 4: return pick_fma_trace<2, 4>(fma, trace);
+        case 8: return pick_fma_trace<2, 8>(fma, trace);
+        case 12: return pick_fma_trace<2, 12>(fma, trace);
+        case 16: return pick_fma_trace<2, 16>(fma, trace);
+        case 24: return pick_fma_trace<2, 24>(fma, trace);
+        case 32: return pick_fma_trace<2, 32>(fma, trace);
+        default: return nullptr;
+    }
+}
+
+struct LaunchCfg {
+    int C, WC, GW, CL, K, RS, Pd, Pr, smem;
+};
+
+sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cfg) {
+    const Options& o = g_opt;
+    int C = (o.packed < 0) ? 2 : (o.packed ? 2 : 1);
+    int W = o.segment_w > 0 ? o.segment_w : 32;
+    if (W % C != 0) return fail(SDTW_E_ARG, "segment width must be a multiple of the chains per lane");
+    int WC = W / C;
+    if (!pick_kernel(C, WC, true, false))
+        return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) +
+                                    (C == 2 ? " (packed: 8,16,24,32,48,64)" : " (scalar: 8,16,32)"));
+    int GW = o.lanes > 0 ? o.lanes : 4;
+    int CL = o.cluster > 0 ? o.cluster : 1;
+    if (GW < 1 || GW > 16 || CL < 1 || CL > 16) return fail(SDTW_E_ARG, "lanes/cluster out of range");
+    int K = o.chunk > 0 ? o.chunk : 32;
+    if (K != 8 && K != 16 && K != 32 && K != 64) return fail(SDTW_E_ARG, "chunk must be 8,16,32,64");
+    if ((32 * C) % K != 0) return fail(SDTW_E_ARG, "chunk must divide 32*chains");
+    const int G = GW * CL;
+    const int64_t V = 32LL * C * G;
+    const int64_t need = V + (int64_t)(G + 1) * K;
+    const int64_t Pd = N > need ? N : need;
+    const int64_t Pr = (ctx.M + V * WC - 1) / (V * WC);
+    if (Pr * Pd + V + 2 * K >= (1LL << 31) || Pr * V * WC >= (1LL << 31))
+        return fail(SDTW_E_ARG, "problem too large for 32-bit step/column counters");
+    const int RS = 4 * K;
+    const sdtw::SmemLayout L = sdtw::smem_layout(C, trace, GW, CL, (int)Pd, RS);
+    if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
+    *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes};
+    (void)Z;
+    return SDTW_OK;
+}
+
+sdtw_status launch_dp(const LaunchCfg& c, bool fma, bool trace, const DpParams& p, cudaStream_t st) {
+    DpKernel k = pick_kernel(c.C, c.WC, fma, trace);
+    CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem));
+    if (c.CL > 8) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t lc;
+    memset(&lc, 0, sizeof(lc));
+    lc.gridDim = dim3((unsigned)(p.Z * c.CL));
+    lc.blockDim = dim3((unsigned)(32 * c.GW));
+    lc.dynamicSmemBytes = (size_t)c.smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)c.CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, k, p));
+    g_launches++;
+    return SDTW_OK;
+}
+
+sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
+                      int64_t* out_start, bool trace) {
+    if (N < 1 || Z < 0) return fail(SDTW_E_ARG, "N must be >= 1 and n_queries >= 0");
+    if (Z > 0 && (!Q || !out_cost || !out_end || (trace && !out_start)))
+        return fail(SDTW_E_ARG, "NULL pointer");
+    if (Z > 0x7fffffff || N > 0x7fffffff) return fail(SDTW_E_ARG, "sizes exceed int32");
+    Ctx* ctx;
+    sdtw_status s = get_ctx(&ctx);
+    if (s != SDTW_OK) return s;
+    if (!ctx->ref) return fail(SDTW_E_NOREF, "no reference set on this device");
+    ctx->last_launches = 0;
+    ctx->last_dp_ms = 0.0;
+    if (Z == 0) return SDTW_OK;
+    const Options o = g_opt;
+    cudaStream_t st = o.stream;
+    const int64_t launches0 = g_launches.load();
+
+    LaunchCfg cfg;
+    s = plan(*ctx, Z, N, trace, &cfg);
+    if (s != SDTW_OK) return s;
+
+    const int kq = ptr_kind(Q), kc = ptr_kind(out_cost), ke = ptr_kind(out_end);
+    const int ks = trace ? ptr_kind(out_start) : 1;
+    if (kq < 0 || kc < 0 || ke < 0 || ks < 0) return fail(SDTW_E_ARG, "device pointer on another device");
+    const size_t nel = (size_t)Z * (size_t)N;
+
+    const float* qd = Q;
+    if (kq == 0) {
+        s = grow(&ctx->ws_q, &ctx->ws_q_n, nel);
+        if (s != SDTW_OK) return s;
+        CK(cudaMemcpyAsync(ctx->ws_q, Q, nel * sizeof(float), cudaMemcpyHostToDevice, st));
+        qd = ctx->ws_q;
+    }
+    CK(cudaMemsetAsync(ctx->flag_d, 0, sizeof(int), st));
+    const float* xd = qd;
+    if (o.normalize) {
+        s = grow(&ctx->ws_x, &ctx->ws_x_n, nel);
+        if (s != SDTW_OK) return s;
+        sdtw::znorm_rows_kernel<<<(unsigned)Z, 256, 0, st>>>(qd, ctx->ws_x, N, 1, ctx->flag_d);
+        xd = ctx->ws_x;
+    } else {
+        sdtw::znorm_rows_kernel<<<(unsigned)Z, 256, 0, st>>>(qd, const_cast<float*>(qd), N, 0, ctx->flag_d);
+    }
+    CK(cudaGetLastError());
+    g_launches++;
+
+    // outputs: direct when device pointers, else staged
+    const bool host_out = (kc == 0 || ke == 0 || ks == 0);
+    float* dc = out_cost;
+    int64_t* de = out_end;
+    int64_t* ds = out_start;
+    if (host_out) {
+        s = grow(&ctx->ws_out, &ctx->ws_out_n, (size_t)Z * 24 + 64);
+        if (s != SDTW_OK) return s;
+        de = reinterpret_cast<int64_t*>(ctx->ws_out);
+        ds = de + Z;
+        dc = reinterpret_cast<float*>(ds + Z);
+    }
+    DpParams p;
+    p.X = xd;
+    p.Y = ctx->ref;
+    p.Malloc = (int)ctx->Malloc;
+    p.Z = (int)Z;
+    p.N = (int)N;
+    p.M = (int)ctx->M;
+    p.Pd = cfg.Pd;
+    p.Pr = cfg.Pr;
+    p.K = cfg.K;
+    p.RS = cfg.RS;
+    p.out_cost = dc;
+    p.out_end = de;
+    p.out_start = trace ? ds : nullptr;
+    p.err_flag = ctx->flag_d;
+    if (o.profile) CK(cudaEventRecord(ctx->ev0, st));
+    s = launch_dp(cfg, o.fma != 0, trace, p, st);
+    if (s != SDTW_OK) return s;
+    if (o.profile) CK(cudaEventRecord(ctx->ev1, st));
+    CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (o.profile) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        ctx->last_dp_ms = ms;
+    }
+    ctx->last_launches = g_launches.load() - launches0;
+    if (*ctx->flag_h) return fail(SDTW_E_NONFINITE, "query batch contains a non-finite sample");
+    if (host_out) {
+        // copy each output to wherever it lives
+        auto cp = [&](void* dst, const void* src, size_t bytes, int kind) -> cudaError_t {
+            return cudaMemcpyAsync(dst, src, bytes, kind ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st);
+        };
+        if (dc != out_cost) CK(cp(out_cost, dc, Z * sizeof(float), kc));
+        if (de != out_end) CK(cp(out_end, de, Z * sizeof(int64_t), ke));
+        if (trace && ds != out_start) CK(cp(out_start, ds, Z * sizeof(int64_t), ks));
+        CK(cudaStreamSynchronize(st));
+    }
+    return SDTW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sdtw_status sdtw_set_reference(const float* Y, int64_t M) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (M < 1 || !Y) return fail(SDTW_E_ARG, "M must be >= 1 and Y non-NULL");
+    if (M > 0x7fffffffLL - 4096) return fail(SDTW_E_ARG, "M exceeds int32 range");
+    Ctx* ctx;
+    sdtw_status s = get_ctx(&ctx);
+    if (s != SDTW_OK) return s;
+    cudaStream_t st = g_opt.stream;
+    const int64_t Malloc = (M + 63) / 64 * 64 + 64;
+    float* buf = nullptr;
+    CK(cudaMalloc(&buf, Malloc * sizeof(float)));
+    const int kind = ptr_kind(Y);
+    if (kind < 0) { cudaFree(buf); return fail(SDTW_E_ARG, "device pointer on another device"); }
+    cudaError_t e = cudaMemcpyAsync(buf, Y, M * sizeof(float),
+                                    kind ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) { cudaFree(buf); return cuda_fail(e, "cudaMemcpyAsync(reference)"); }
+    const int nparts = 1184;
+    cudaMemsetAsync(ctx->flag_d, 0, sizeof(int), st);
+    sdtw::ref_partials_kernel<<<nparts, 256, 0, st>>>(buf, M, ctx->ws_part, ctx->flag_d);
+    sdtw::ref_stats_kernel<<<1, 256, 0, st>>>(ctx->ws_part, nparts, M, ctx->ws_part + 2 * 4096);
+    const int norm = g_opt.normalize;
+    sdtw::ref_apply_kernel<<<1184, 256, 0, st>>>(buf, M, Malloc, ctx->ws_part + 2 * 4096, norm, buf);
+    g_launches += 3;
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { cudaFree(buf); return cuda_fail(e, "set_reference kernels"); }
+    if (*ctx->flag_h) { cudaFree(buf); return fail(SDTW_E_NONFINITE, "reference contains a non-finite sample"); }
+    if (ctx->ref) cudaFree(ctx->ref);
+    ctx->ref = buf;
+    ctx->M = M;
+    ctx->Malloc = Malloc;
+    ctx->ref_normalized = norm;
+    return SDTW_OK;
+}
+
+sdtw_status sdtw_batch(const float* Q, int64_t n_queries, int64_t N, float* out_cost, int64_t* out_end) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return run_batch(Q, n_queries, N, out_cost, out_end, nullptr, false);
+}
+
+sdtw_status sdtw_traceback(const float* Q, int64_t n_queries, int64_t N, float* out_cost, int64_t* out_end,
+                           int64_t* out_start) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return run_batch(Q, n_queries, N, out_cost, out_end, out_start, true);
+}
+
+sdtw_status sdtw_znormalize(const float* in, int64_t n_series, int64_t len, float* out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (n_series < 0 || len < 1) return fail(SDTW_E_ARG, "len must be >= 1 and n_series >= 0");
+    if (n_series > 0 && (!in || !out)) return fail(SDTW_E_ARG, "NULL pointer");
+    if (n_series > 0x7fffffff) return fail(SDTW_E_ARG, "n_series exceeds int32");
+    Ctx* ctx;
+    sdtw_status s = get_ctx(&ctx);
+    if (s != SDTW_OK) return s;
+    if (n_series == 0) return SDTW_OK;
+    cudaStream_t st = g_opt.stream;
+    const int ki = ptr_kind(in), ko = ptr_kind(out);
+    if (ki < 0 || ko < 0) return fail(SDTW_E_ARG, "device pointer on another device");
+    const size_t nel = (size_t)n_series * (size_t)len;
+    const float* id = in;
+    if (ki == 0) {
+        s = grow(&ctx->ws_q, &ctx->ws_q_n, nel);
+        if (s != SDTW_OK) return s;
+        CK(cudaMemcpyAsync(ctx->ws_q, in, nel * sizeof(float), cudaMemcpyHostToDevice, st));
+        id = ctx->ws_q;
+    }
+    float* od = out;
+    if (ko == 0) {
+        s = grow(&ctx->ws_x, &ctx->ws_x_n, nel);
+        if (s != SDTW_OK) return s;
+        od = ctx->ws_x;
+    }
+    // write to a staging buffer when output is device memory too, so that no
+    // partial result is written if a sample is non-finite
+    if (ko == 1) {
+        s = grow(&ctx->ws_x, &ctx->ws_x_n, nel);
+        if (s != SDTW_OK) return s;
+        od = ctx->ws_x;
+    }
+    CK(cudaMemsetAsync(ctx->flag_d, 0, sizeof(int), st));
+    sdtw::znorm_rows_kernel<<<(unsigned)n_series, 256, 0, st>>>(id, od, len, 1, ctx->flag_d);
+    CK(cudaGetLastError());
+    g_launches++;
+    CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (*ctx->flag_h) return fail(SDTW_E_NONFINITE, "input contains a non-finite sample");
+    CK(cudaMemcpyAsync(out, od, nel * sizeof(float), ko ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return SDTW_OK;
+}
+
+sdtw_status sdtw_set_option(int key, int64_t v) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    switch (key) {
+        case SDTW_OPT_NORMALIZE: if (v != 0 && v != 1) break; g_opt.normalize = (int)v; return SDTW_OK;
+        case SDTW_OPT_FMA: if (v != 0 && v != 1) break; g_opt.fma = (int)v; return SDTW_OK;
+        case SDTW_OPT_SEGMENT_W: if (v < 0 || v > 64) break; g_opt.segment_w = (int)v; return SDTW_OK;
+        case SDTW_OPT_LANES: if (v < 0 || v > 16) break; g_opt.lanes = (int)v; return SDTW_OK;
+        case SDTW_OPT_CLUSTER: if (v < 0 || v > 16) break; g_opt.cluster = (int)v; return SDTW_OK;
+        case SDTW_OPT_STREAM: g_opt.stream = reinterpret_cast<cudaStream_t>(v); return SDTW_OK;
+        case SDTW_OPT_PACKED: if (v < -1 || v > 1) break; g_opt.packed = (int)v; return SDTW_OK;
+        case SDTW_OPT_CHUNK: if (v < 0 || v > 64) break; g_opt.chunk = (int)v; return SDTW_OK;
+        case SDTW_OPT_PROFILE: if (v != 0 && v != 1) break; g_opt.profile = (int)v; return SDTW_OK;
+        default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
+    }
+    return fail(SDTW_E_ARG, "bad value for option " + std::to_string(key));
+}
+
+sdtw_status sdtw_get_option(int key, int64_t* v) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!v) return fail(SDTW_E_ARG, "NULL pointer");
+    switch (key) {
+        case SDTW_OPT_NORMALIZE: *v = g_opt.normalize; return SDTW_OK;
+        case SDTW_OPT_FMA: *v = g_opt.fma; return SDTW_OK;
+        case SDTW_OPT_SEGMENT_W: *v = g_opt.segment_w; return SDTW_OK;
+        case SDTW_OPT_LANES: *v = g_opt.lanes; return SDTW_OK;
+        case SDTW_OPT_CLUSTER: *v = g_opt.cluster; return SDTW_OK;
+        case SDTW_OPT_STREAM: *v = reinterpret_cast<int64_t>(g_opt.stream); return SDTW_OK;
+        case SDTW_OPT_PACKED: *v = g_opt.packed; return SDTW_OK;
+        case SDTW_OPT_CHUNK: *v = g_opt.chunk; return SDTW_OK;
+        case SDTW_OPT_PROFILE: *v = g_opt.profile; return SDTW_OK;
+        default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
+    }
+}
+
+sdtw_status sdtw_profile(double* dp_ms, int64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    Ctx* ctx;
+    sdtw_status s = get_ctx(&ctx);
+    if (s != SDTW_OK) return s;
+    if (dp_ms) *dp_ms = ctx->last_dp_ms;
+    if (launches) *launches = ctx->last_launches;
+    return SDTW_OK;
+}
+
+int64_t sdtw_launch_count(void) { return g_launches.load(); }
+
+const char* sdtw_last_error(void) { return g_err.c_str(); }
+
+void sdtw_release(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return;
+    Ctx& c = g_ctx[dev];
+    if (!c.init) return;
+    cudaDeviceSynchronize();
+    cudaFree(c.ref);
+    cudaFree(c.ws_q);
+    cudaFree(c.ws_x);
+    cudaFree(c.ws_out);
+    cudaFree(c.ws_part);
+    cudaFree(c.flag_d);
+    cudaFreeHost(c.flag_h);
+    cudaEventDestroy(c.ev0);
+    cudaEventDestroy(c.ev1);
+    c = Ctx();
+}
+
+int sdtw_version(void) { return 1; }
+
+}  // extern "C"

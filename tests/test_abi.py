@@ -1,0 +1,97 @@
+"""CPU-side checks of the C-ABI library: it builds for sm_100a, loads, exports every
+symbol include/sdtw.h declares, validates options, and fails loudly (no CPU
+fallback) when no GPU is present."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "sdtw.h")).read()
+    return sorted(set(re.findall(r"\b(sdtw_[a-z_]+)\s*\(", hdr)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2403_06931_b200 import build
+    path = build.build()
+    return ctypes.CDLL(path)
+
+
+def test_header_declares_the_survey_entry_points():
+    syms = _declared_symbols()
+    for s in ("sdtw_set_reference", "sdtw_batch", "sdtw_traceback", "sdtw_znormalize",
+              "sdtw_set_option", "sdtw_last_error", "sdtw_release"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for s in _declared_symbols():
+        assert hasattr(lib, s), s
+    import paper_2403_06931_b200 as sd
+    assert set(sd.EXPORTED_SYMBOLS) == set(_declared_symbols())
+
+
+def test_library_is_sm100a_native(lib):
+    from paper_2403_06931_b200 import build
+    out = subprocess.run(["cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", build.LIB], capture_output=True, text=True).stdout
+    # the packed hot loop: FADD2 + FFMA2 (Blackwell f32x2) and the 3-way FMNMX3
+    assert "FFMA2" in sass and "FADD2" in sass and "FMNMX3" in sass
+
+
+def test_version_and_options(lib):
+    import paper_2403_06931_b200 as sd
+    assert sd.version() == 1
+    old = sd.get_option(sd.OPT_FMA)
+    sd.set_option(sd.OPT_FMA, 0)
+    assert sd.get_option(sd.OPT_FMA) == 0
+    sd.set_option(sd.OPT_FMA, old)
+    with pytest.raises(sd.SdtwError) as e:
+        sd.set_option(999, 1)
+    assert e.value.status == sd.E_ARG
+    with pytest.raises(sd.SdtwError):
+        sd.set_option(sd.OPT_NORMALIZE, 7)
+    with sd.options(OPT_SEGMENT_W=16):
+        assert sd.get_option(sd.OPT_SEGMENT_W) == 16
+    assert sd.get_option(sd.OPT_SEGMENT_W) == 0
+
+
+def test_no_gpu_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import numpy as np
+    import paper_2403_06931_b200 as sd
+    with pytest.raises(sd.SdtwError) as e:
+        sd.set_reference(np.zeros(16, np.float32))
+    assert e.value.status == sd.E_CUDA
+    with pytest.raises(sd.SdtwError):
+        sd.batch(np.zeros((2, 4), np.float32))
+
+
+def test_argument_errors_before_device(lib):
+    import numpy as np
+    import paper_2403_06931_b200 as sd
+    with pytest.raises(sd.SdtwError) as e:
+        sd.set_reference(np.zeros(0, np.float32))
+    assert e.value.status == sd.E_ARG
+    rc = lib.sdtw_batch(None, ctypes.c_int64(1), ctypes.c_int64(0), None, None)
+    assert rc == sd.E_ARG
+
+
+def test_oracle_not_imported_by_product():
+    """The product package never imports the oracle (no CPU fallback path)."""
+    pkg = os.path.join(ROOT, "paper_2403_06931_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "sdtw_oracle" not in txt, f

@@ -1,0 +1,78 @@
+"""World-size-2 gloo test of the query-sharded multi-GPU host logic on CPU.
+
+The per-rank compute is injected (the CPU oracle -- tests may call it) so that the
+sharding, padding, record packing and the one all-gather are exercised without
+a GPU; results must equal the single-process oracle bit for bit, including a
+batch size not divisible by the world size and an empty shard."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, Z, traceback, out_q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2403_06931_b200.distributed import distributed_batch
+        rng = np.random.default_rng(5)
+        Y = rng.standard_normal(700).astype(np.float32)
+        Q = rng.standard_normal((Z, 24)).astype(np.float32)
+
+        def fn(Qs):
+            r = oracle.sdtw(np.asarray(Qs), Y, start=traceback, threads=1)
+            return (r["cost"], r["end"], r["start"]) if traceback else (r["cost"], r["end"])
+
+        cost, end, start = distributed_batch(Q, traceback=traceback, fn=fn)
+        out_q.put((rank, cost, end, start))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("Z,traceback", [(7, False), (8, True), (1, True)])
+def test_gloo_world2_matches_single_process(Z, traceback):
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, Z, traceback, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(5)
+    Y = rng.standard_normal(700).astype(np.float32)
+    Q = rng.standard_normal((Z, 24)).astype(np.float32)
+    ref = oracle.sdtw(Q, Y, start=True)
+    for _, cost, end, start in res:
+        assert np.array_equal(cost, ref["cost"])
+        assert np.array_equal(end, ref["end"])
+        if traceback:
+            assert np.array_equal(start, ref["start"])
+
+
+def test_shard_bounds_cover_everything_once():
+    from paper_2403_06931_b200.distributed import shard_bounds
+    for Z in (0, 1, 7, 8, 512, 513):
+        for world in (1, 2, 3, 8):
+            seen = []
+            for r in range(world):
+                lo, hi, per = shard_bounds(Z, world, r)
+                assert 0 <= hi - lo <= per
+                seen.extend(range(lo, hi))
+            assert seen == list(range(Z))
