@@ -29,6 +29,7 @@
 //    (priority diag > up > left on equality; reading G6).
 #pragma once
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -61,9 +62,24 @@ __device__ __forceinline__ int ld_acquire_cluster(const int* p) {
     asm volatile("ld.acquire.cluster.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void spin_until_geq(const int* p, int need) {
+// Wait until *p >= need.  A watchdog turns a protocol bug into a diagnosable trap
+// instead of a hung GPU (never reached in a correct run: every wait is bounded by
+// the ring's progress).
+__device__ __noinline__ void spin_slow(const int* p, int need, int tag) {
+    long long n = 0;
+    int v;
+    while ((v = ld_acquire_cluster(p)) < need) {
+        __nanosleep(32);
+        if (++n == (1LL << 25)) {
+            printf("sdtw watchdog: block %d thread %d tag %d waits *p=%d >= %d\n", (int)blockIdx.x,
+                   (int)threadIdx.x, tag, v, need);
+            __trap();
+        }
+    }
+}
+__device__ __forceinline__ void spin_until_geq(const int* p, int need, int tag = 0) {
     if (ld_acquire_cluster(p) >= need) return;
-    while (ld_acquire_cluster(p) < need) __nanosleep(20);
+    spin_slow(p, need, tag);
 }
 
 __device__ __forceinline__ unsigned long long pk2(float2 a) {
@@ -322,18 +338,23 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     int p0 = (b0 < 0) ? -1 : 0;
     int r0 = (b0 < 0) ? b0 + Pd : 0;
 
+    // warp g runs steps [32*C*g, 32*C*g + span): its lanes' bands cover [0, Pr*Pd)
+    const int span = (32 * C - 1 + Mtot_bands + K - 1) / K * K;
     const int t_begin = 32 * C * gw;
-    const int t_last = t_begin + 32 * C - 1 + Mtot_bands - 1;  // inclusive
-    const int t_end = ((t_last + 1) + K - 1) / K * K;
+    const int t_end = t_begin + span;
+    // a predecessor never publishes past its own end: the successor's trailing
+    // (idle-band) chunks must not wait for more
+    const int pred_end = t_end - 32 * C;                 // = t_end of warp gw-1
+    const int last_end = 32 * C * (G - 1) + span;        // = t_end of warp G-1
     const unsigned FULL = 0xffffffffu;
 
     for (int t0 = t_begin; t0 < t_end; t0 += K) {
         // ---- chunk-level flow control (one lane each), then converge
         if (lane == 0) {
-            if (gw > 0) spin_until_geq(pp + warp, t0 + K - 1);
-            else if (t0 + K - 1 >= Pd) spin_until_geq(pp, t0 + K - Pd + u_last);
+            if (gw > 0) spin_until_geq(pp + warp, min(t0 + K - 1, pred_end), 1);
+            else if (t0 + K - 1 >= Pd) spin_until_geq(pp, min(t0 + K - Pd + u_last, last_end), 2);
         }
-        if (lane == 31 && has_succ_ring) spin_until_geq(cp + warp, t0 + K - RS + 1);
+        if (lane == 31 && has_succ_ring) spin_until_geq(cp + warp, t0 + K - RS + 1, 3);
         __syncwarp();
 
 #pragma unroll 1
