@@ -47,8 +47,8 @@ enum {
                                0: raw samples */
     SDTW_OPT_FMA = 2,       /* 1 (default): cell = fmaf(t,t,m); 0: fl(fl(t*t)+m) -- both
                                bit-exact with the oracle in the same mode */
-    SDTW_OPT_SEGMENT_W = 3, /* reference columns per lane ("segment width");
-                               0 = auto */
+    SDTW_OPT_SEGMENT_W = 3, /* reference columns per lane ("segment width"):
+                               packed 6, 14, 30 (default), 62; scalar 7, 15, 31; 0 = auto */
     SDTW_OPT_LANES = 4,     /* warps per CTA in one query ring; 0 = auto */
     SDTW_OPT_CLUSTER = 5,   /* CTAs per query (thread-block cluster, DSMEM handoff); 0 = auto */
     SDTW_OPT_STREAM = 6,    /* cudaStream_t as int64 (0 = legacy default stream) */

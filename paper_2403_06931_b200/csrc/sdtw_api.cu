@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <algorithm>
 
 namespace {
 
@@ -126,19 +127,17 @@ DpKernel pick_fma_trace(bool fma, bool trace) {
 DpKernel pick_kernel(int C, int WC, bool fma, bool trace) {
     if (C == 1) {
         switch (WC) {
-            case 8: return pick_fma_trace<1, 8>(fma, trace);
-            case 16: return pick_fma_trace<1, 16>(fma, trace);
-            case 32: return pick_fma_trace<1, 32>(fma, trace);
+            case 7: return pick_fma_trace<1, 7>(fma, trace);
+            case 15: return pick_fma_trace<1, 15>(fma, trace);
+            case 31: return pick_fma_trace<1, 31>(fma, trace);
             default: return nullptr;
         }
     }
     switch (WC) {
-        case 4: return pick_fma_trace<2, 4>(fma, trace);
-        case 8: return pick_fma_trace<2, 8>(fma, trace);
-        case 12: return pick_fma_trace<2, 12>(fma, trace);
-        case 16: return pick_fma_trace<2, 16>(fma, trace);
-        case 24: return pick_fma_trace<2, 24>(fma, trace);
-        case 32: return pick_fma_trace<2, 32>(fma, trace);
+        case 3: return pick_fma_trace<2, 3>(fma, trace);
+        case 7: return pick_fma_trace<2, 7>(fma, trace);
+        case 15: return pick_fma_trace<2, 15>(fma, trace);
+        case 31: return pick_fma_trace<2, 31>(fma, trace);
         default: return nullptr;
     }
 }
@@ -150,18 +149,19 @@ struct LaunchCfg {
 sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cfg) {
     const Options& o = g_opt;
     int C = (o.packed < 0) ? 2 : (o.packed ? 2 : 1);
-    int W = o.segment_w > 0 ? o.segment_w : 32;
+    int W = o.segment_w > 0 ? o.segment_w : (C == 2 ? 30 : 31);
     if (W % C != 0) return fail(SDTW_E_ARG, "segment width must be a multiple of the chains per lane");
     int WC = W / C;
     if (!pick_kernel(C, WC, true, false))
         return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) +
-                                    (C == 2 ? " (packed: 8,16,24,32,48,64)" : " (scalar: 8,16,32)"));
+                                    (C == 2 ? " (packed: 6,14,30,62)" : " (scalar: 7,15,31)"));
     int GW = o.lanes > 0 ? o.lanes : 4;
     int CL = o.cluster > 0 ? o.cluster : 1;
-    if (GW < 1 || GW > 16 || CL < 1 || CL > 16) return fail(SDTW_E_ARG, "lanes/cluster out of range");
-    int K = o.chunk > 0 ? o.chunk : 32;
-    if (K != 8 && K != 16 && K != 32 && K != 64) return fail(SDTW_E_ARG, "chunk must be 8,16,32,64");
-    if ((32 * C) % K != 0) return fail(SDTW_E_ARG, "chunk must divide 32*chains");
+    if (GW < 1 || GW > 8 || CL < 1 || CL > 16) return fail(SDTW_E_ARG, "lanes (1..8) / cluster (1..16) out of range");
+    // chunk = whole rotation periods (U = WC+1 steps), about the requested size
+    const int U = WC + 1;
+    const int Kreq = o.chunk > 0 ? o.chunk : 32;
+    const int K = U * std::max(1, (Kreq + U / 2) / U);
     const int G = GW * CL;
     const int64_t V = 32LL * C * G;
     const int64_t need = V + (int64_t)(G + 1) * K;
@@ -169,7 +169,8 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     const int64_t Pr = (ctx.M + V * WC - 1) / (V * WC);
     if (Pr * Pd + V + 2 * K >= (1LL << 31) || Pr * V * WC >= (1LL << 31))
         return fail(SDTW_E_ARG, "problem too large for 32-bit step/column counters");
-    const int RS = 4 * K;
+    int RS = 1;
+    while (RS < 4 * K) RS <<= 1;
     const sdtw::SmemLayout L = sdtw::smem_layout(C, trace, GW, CL, (int)Pd, RS);
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
     *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes};
@@ -404,7 +405,7 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_CLUSTER: if (v < 0 || v > 16) break; g_opt.cluster = (int)v; return SDTW_OK;
         case SDTW_OPT_STREAM: g_opt.stream = reinterpret_cast<cudaStream_t>(v); return SDTW_OK;
         case SDTW_OPT_PACKED: if (v < -1 || v > 1) break; g_opt.packed = (int)v; return SDTW_OK;
-        case SDTW_OPT_CHUNK: if (v < 0 || v > 64) break; g_opt.chunk = (int)v; return SDTW_OK;
+        case SDTW_OPT_CHUNK: if (v < 0 || v > 256) break; g_opt.chunk = (int)v; return SDTW_OK;
         case SDTW_OPT_PROFILE: if (v != 0 && v != 1) break; g_opt.profile = (int)v; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }

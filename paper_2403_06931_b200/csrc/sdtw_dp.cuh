@@ -31,6 +31,7 @@
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace sdtw {
@@ -120,30 +121,9 @@ __device__ __forceinline__ bool better(float ca, int ja, float cb, int jb) {
     return ca < cb || (ca == cb && ja < jb);
 }
 
-// Load the WC reference samples of strip `strip` (+inf outside [0, Malloc)).
-template <int WC>
-__device__ __forceinline__ void load_strip(const float* __restrict__ Y, int Malloc, long strip,
-                                           float (&y)[WC]) {
-    const long col0 = strip * WC;
-#pragma unroll
-    for (int k = 0; k < WC / 4; ++k) {
-        const long c = col0 + 4 * k;
-        float4 v;
-        if (c + 4 <= (long)Malloc) {
-            v = __ldg(reinterpret_cast<const float4*>(Y + c));
-        } else {
-            v = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
-        }
-        y[4 * k + 0] = v.x;
-        y[4 * k + 1] = v.y;
-        y[4 * k + 2] = v.z;
-        y[4 * k + 3] = v.w;
-    }
-}
-
 // Shared-memory carve-up (dynamic).  Returns total bytes.
 struct SmemLayout {
-    int off_ctr, off_red, off_x, off_bnd, off_ring, bytes;
+    int off_ctr, off_red, off_inf, off_x, off_bnd, off_ring, bytes;
 };
 __host__ __device__ inline SmemLayout smem_layout(int C, bool trace, int GW, int CL, int Pd, int RS) {
     SmemLayout L;
@@ -151,8 +131,9 @@ __host__ __device__ inline SmemLayout smem_layout(int C, bool trace, int GW, int
     int o = 0;
     L.off_ctr = o;  o += 2 * 32 * 4;                   // pp[32], cp[32]
     L.off_red = o;  o += 16 * (32 + 16);               // per-warp + per-rank partials
+    L.off_inf = o;  o += 32 * 8;                        // +inf inbox entries (round 0)
     o = (o + 15) & ~15;
-    L.off_x = o;    o += Pd * C * 4;
+    L.off_x = o;    o += (Pd + 1) * C * 4;
     o = (o + 15) & ~15;
     L.off_bnd = o;  o += Pd * ent;
     o = (o + 15) & ~15;
@@ -164,16 +145,9 @@ __host__ __device__ inline SmemLayout smem_layout(int C, bool trace, int GW, int
 
 struct Partial { float cost; int col; int start; int pad; };
 
-// Register strip of one lane: C chains x WC columns of D (previous row) and y.
-// C == 2 keeps (chain0, chain1) pairs in aligned 64-bit registers so that FADD2 /
-// FFMA2 read and write them in place (no pair-building moves in the hot loop).
-template <int C, int WC> struct Strip;
-template <int WC> struct Strip<1, WC> {
-    float D[WC], Y[WC];
-    __device__ __forceinline__ float d(int, int w) const { return D[w]; }
-    __device__ __forceinline__ void set_d(int, int w, float v) { D[w] = v; }
-    __device__ __forceinline__ void set_y(int, int w, float v) { Y[w] = v; }
-};
+// ----------------------------------------------------------------------------
+// Register state of one lane.  C == 2 keeps (chain0, chain1) pairs in aligned
+// 64-bit registers so that FADD2 / FFMA2 read and write them in place.
 __device__ __forceinline__ float lo32(unsigned long long r) {
     float a, b;
     asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
@@ -189,58 +163,230 @@ __device__ __forceinline__ unsigned long long pk(float a, float b) {
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
     return r;
 }
-template <int WC> struct Strip<2, WC> {
-    unsigned long long D[WC], Y[WC];
-    __device__ __forceinline__ float d(int c, int w) const { return c ? hi32(D[w]) : lo32(D[w]); }
-    __device__ __forceinline__ void set_d(int c, int w, float v) {
-        D[w] = c ? pk(lo32(D[w]), v) : pk(v, hi32(D[w]));
+
+// A lane's row state lives in a ROTATING register file of U = WC+1 slots per
+// chain (pairs of chains packed in 64-bit registers when C == 2): each cell's new
+// value is written into the slot of its diag input, which dies at that cell, so
+// the row moves one slot down per step and returns to its origin after U steps.
+// The fast loop is unrolled U steps so every slot index is a compile-time
+// constant and no register-to-register moves are needed.
+template <int C> struct RegT { using T = float; };
+template <> struct RegT<2> { using T = unsigned long long; };
+
+template <int C, int WC, bool TRACE> struct RotRow {
+    static constexpr int U = WC + 1;
+    typename RegT<C>::T D[U];
+    int S[TRACE ? C : 1][TRACE ? U : 1];
+    // element w of the row when the rotation offset is h (row at slots (w - h) mod U)
+    __device__ __forceinline__ static constexpr int slot(int w, int h) { return ((w - h) % U + U) % U; }
+    __device__ __forceinline__ float d(int c, int w, int h = 0) const {
+        if constexpr (C == 1) return D[slot(w, h)];
+        else return c ? hi32(D[slot(w, h)]) : lo32(D[slot(w, h)]);
     }
-    __device__ __forceinline__ void set_y(int c, int w, float v) {
-        Y[w] = c ? pk(lo32(Y[w]), v) : pk(v, hi32(Y[w]));
+    __device__ __forceinline__ void set_d(int c, int w, float v, int h = 0) {
+        if constexpr (C == 1) D[slot(w, h)] = v;
+        else {
+            const int k = slot(w, h);
+            D[k] = c ? pk(lo32(D[k]), v) : pk(v, hi32(D[k]));
+        }
+    }
+    __device__ __forceinline__ int s(int c, int w, int h = 0) const {
+        if constexpr (TRACE) return S[c][slot(w, h)];
+        else return 0;
+    }
+    __device__ __forceinline__ void set_s(int c, int w, int v, int h = 0) {
+        if constexpr (TRACE) S[c][slot(w, h)] = v;
     }
 };
+template <int C, int WC> struct Ys;
+template <int WC> struct Ys<1, WC> {
+    float Y[WC];
+    __device__ __forceinline__ void set(int, int w, float v) { Y[w] = v; }
+};
+template <int WC> struct Ys<2, WC> {
+    unsigned long long Y[WC];
+    __device__ __forceinline__ void set(int c, int w, float v) { Y[w] = c ? pk(lo32(Y[w]), v) : pk(v, hi32(Y[w])); }
+};
 
-// New strip for chain c (round transition): reload y, virtual row -1 = 0.
+// Per-lane scalars carried from step to step.
+template <int C> struct LaneScalars {
+    float prevleft[C];   // left input of the previous row (the next row's diag at column 0)
+    int prevleft_s[C];
+    float right0;        // C == 2: chain 0's right edge -> chain 1's left at the next step
+    int right0_s;
+    float outv;          // right edge of the last chain (to lane+1 / next warp)
+    int outs;
+};
+
+// One row of the lane's strips (Eq. 1) at rotation offset H: reads the
+// row at offset H, leaves the new row at offset H+1.
+// C == 1: per cell FADD, FMNMX3, FFMA (3 SASS).  C == 2: per cell pair FADD2,
+// 2x FMNMX3, FFMA2 (2 SASS/cell).  xx: row sample(s); lin: chain 0's left input.
+template <int C, int WC, bool FMA, bool TRACE, int H>
+__device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, WC>& Y, unsigned long long xx,
+                                          float lin, int lins, LaneScalars<C>& ls) {
+    using RR = RotRow<C, WC, TRACE>;
+    if constexpr (C == 1) {
+        const float xv = __uint_as_float((unsigned)xx);
+        float left = lin, diag = ls.prevleft[0];
+        int sl = lins, sd = ls.prevleft_s[0];
+        ls.prevleft[0] = lin;
+        ls.prevleft_s[0] = lins;
+#pragma unroll
+        for (int w = 0; w < WC; ++w) {
+            const int ku = RR::slot(w, H), kd = RR::slot(w - 1, H);   // up slot; diag slot (= output slot)
+            const float up = R.D[ku];
+            const float dg = (w == 0) ? diag : R.D[kd];
+            const float m = min3f(dg, up, left);
+            const float v = cell1<FMA>(xv, Y.Y[w], m);
+            if constexpr (TRACE) {
+                const int su = R.S[0][ku];
+                const int sdg = (w == 0) ? sd : R.S[0][kd];
+                const int sv = (dg == m) ? sdg : ((up == m) ? su : sl);
+                R.S[0][kd] = sv;
+                sl = sv;
+            }
+            R.D[kd] = v;
+            left = v;
+        }
+        ls.outv = left;
+        ls.outs = sl;
+    } else {
+        float l0 = lin, l1 = ls.right0;
+        const float pd0 = ls.prevleft[0], pd1 = ls.prevleft[1];
+        const int psd0 = ls.prevleft_s[0], psd1 = ls.prevleft_s[1];
+        int sl0 = lins, sl1 = ls.right0_s;
+        ls.prevleft[0] = l0;
+        ls.prevleft[1] = l1;
+        ls.prevleft_s[0] = sl0;
+        ls.prevleft_s[1] = sl1;
+#pragma unroll
+        for (int w = 0; w < WC; ++w) {
+            const int ku = RR::slot(w, H), kd = RR::slot(w - 1, H);
+            const float u0v = lo32(R.D[ku]), u1v = hi32(R.D[ku]);
+            const float d0 = (w == 0) ? pd0 : lo32(R.D[kd]);
+            const float d1 = (w == 0) ? pd1 : hi32(R.D[kd]);
+            const float m0 = min3f(d0, u0v, l0);
+            const float m1 = min3f(d1, u1v, l1);
+            unsigned long long tt, vv;
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(xx), "l"(Y.Y[w]));
+            if (FMA) {
+                asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(vv) : "l"(tt), "l"(pk(m0, m1)));
+            } else {
+                const float t0v = lo32(tt), t1v = hi32(tt);
+                vv = pk(__fadd_rn(__fmul_rn(t0v, t0v), m0), __fadd_rn(__fmul_rn(t1v, t1v), m1));
+            }
+            if constexpr (TRACE) {
+                const int su0 = R.S[0][ku], su1 = R.S[1][ku];
+                const int sd0 = (w == 0) ? psd0 : R.S[0][kd];
+                const int sd1 = (w == 0) ? psd1 : R.S[1][kd];
+                const int sv0 = (d0 == m0) ? sd0 : ((u0v == m0) ? su0 : sl0);
+                const int sv1 = (d1 == m1) ? sd1 : ((u1v == m1) ? su1 : sl1);
+                R.S[0][kd] = sv0;
+                R.S[1][kd] = sv1;
+                sl0 = sv0;
+                sl1 = sv1;
+            }
+            R.D[kd] = vv;
+            l0 = lo32(vv);
+            l1 = hi32(vv);
+        }
+        ls.right0 = l0;
+        ls.right0_s = sl0;
+        ls.outv = l1;
+        ls.outs = sl1;
+    }
+}
+
+// Load the WC reference samples of strip `strip` (+inf beyond Malloc).
+template <int WC>
+__device__ __forceinline__ void load_strip_any(const float* __restrict__ Yg, int Malloc, long strip, float (&y)[WC]) {
+    const long col0 = strip * WC;
+#pragma unroll
+    for (int w = 0; w < WC; ++w) y[w] = (col0 + w < (long)Malloc) ? __ldg(Yg + col0 + w) : INFINITY;
+}
+
+// Round transition of chain c at rotation offset 0: new strip (reload y),
+// virtual row -1 = 0.
 template <int C, int WC, bool TRACE>
-__device__ __forceinline__ void enter_strip(Strip<C, WC>& st, int (&S)[TRACE ? C : 1][TRACE ? WC : 1],
-                                            int c, long strip, bool live, const DpParams& P,
-                                            float& prevleft, int& prevleft_s) {
+__device__ __forceinline__ void enter_strip(RotRow<C, WC, TRACE>& row, Ys<C, WC>& Y, int c, long strip, bool live,
+                                            const float* __restrict__ Yg, int Malloc, LaneScalars<C>& ls) {
     float y[WC];
-    if (live) load_strip<WC>(P.Y, P.Malloc, strip, y);
+    if (live) load_strip_any<WC>(Yg, Malloc, strip, y);
     else {
 #pragma unroll
         for (int w = 0; w < WC; ++w) y[w] = INFINITY;
     }
 #pragma unroll
     for (int w = 0; w < WC; ++w) {
-        st.set_y(c, w, y[w]);
-        st.set_d(c, w, 0.0f);
-        if constexpr (TRACE) S[c][w] = (int)(strip * WC) + w + 1;   // S(-1, j) = j+1
+        Y.set(c, w, y[w]);
+        row.set_d(c, w, 0.0f);
+        row.set_s(c, w, (int)(strip * WC) + w + 1);   // S(-1, j) = j+1, so row 0 gets S = j
     }
-    prevleft = 0.0f;                    // D(-1, col0-1) = 0
-    prevleft_s = (int)(strip * WC);     // so that row 0 gets S = j
+    ls.prevleft[c] = 0.0f;                // D(-1, col0-1) = 0
+    ls.prevleft_s[c] = (int)(strip * WC);
 }
 
+// Fold the last row of chain c (rotation offset 0) into (best, bestcol, beststart):
+// strict '<' keeps the smallest column on ties (strips are visited in increasing
+// column order).
 template <int C, int WC, bool TRACE>
-__device__ __forceinline__ void fold_last_row(const Strip<C, WC>& st, const int (&S)[TRACE ? C : 1][TRACE ? WC : 1],
-                                              int c, int col0, float& best, int& bestcol, int& beststart) {
+__device__ __forceinline__ void fold_last_row(const RotRow<C, WC, TRACE>& row, int c, int col0, float& best,
+                                              int& bestcol, int& beststart) {
 #pragma unroll
     for (int w = 0; w < WC; ++w) {
-        const float v = st.d(c, w);
+        const float v = row.d(c, w);
         if (v < best) {
             best = v;
             bestcol = col0 + w;
-            if constexpr (TRACE) beststart = S[c][w];
+            beststart = row.s(c, w);
         }
     }
+}
+
+// Move the row from rotation offset 1 back to offset 0 (slow path only).
+template <int C, int WC, bool TRACE>
+__device__ __forceinline__ void unrotate1(RotRow<C, WC, TRACE>& R) {
+    using RR = RotRow<C, WC, TRACE>;
+    RotRow<C, WC, TRACE> T;
+#pragma unroll
+    for (int w = 0; w < RR::U; ++w) {
+        T.D[w] = R.D[RR::slot(w, 1)];
+        if constexpr (TRACE) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) T.S[c][w] = R.S[c][RR::slot(w, 1)];
+        }
+    }
+    R = T;
+}
+
+template <int I, int N_, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (I < N_) {
+        f(std::integral_constant<int, I>{});
+        static_for<I + 1, N_>(f);
+    }
+}
+
+// index of the (x_r, x_{r-1}) pair of row r in the parity-split layout
+__host__ __device__ __forceinline__ int xpair_index(int r, int Pd) { return (r & 1) * ((Pd + 1) >> 1) + (r >> 1); }
+
+// floor-mod
+__device__ __forceinline__ int fmod_pos(int a, int m) { int r = a % m; return r < 0 ? r + m : r; }
+// does the band interval [blo, blo+len) contain a band whose row (band mod Pd) == row?
+__device__ __forceinline__ bool hits_row(int blo, int len, int row, int Pd) {
+    return fmod_pos(row - blo, Pd) < len;
 }
 
 template <int C, int WC, bool FMA, bool TRACE>
 __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     static_assert(C == 1 || C == 2, "C");
-    static_assert(WC % 4 == 0, "WC");
+    static_assert(((WC + 1) & WC) == 0 && (32 * C) % (WC + 1) == 0,
+                  "rotation period U = WC+1 must be a power of two dividing 32*C");
     extern __shared__ __align__(16) unsigned char smem[];
     using E = Entry<TRACE>;
+    using RowT = RotRow<C, WC, TRACE>;
+    constexpr int U = RowT::U;
 
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = (int)cluster.num_blocks();
@@ -261,15 +407,18 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     E* bnd = reinterpret_cast<E*>(smem + L.off_bnd);
     E* ring = reinterpret_cast<E*>(smem + L.off_ring);
     Partial* red = reinterpret_cast<Partial*>(smem + L.off_red);
+    E* infs = reinterpret_cast<E*>(smem + L.off_inf);
 
     // ---- prologue: query -> smem (pairs (x_r, x_{r-1 mod Pd}) when C == 2), rings, counters
     const float* xq = P.X + (long)q * N;
     for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
         const float a = (r < N) ? xq[r] : 0.0f;
         if (C == 2) {
+            // pairs (x_r, x_{r-1}); even rows then odd rows so that a warp's lanes
+            // (rows r, r-2, r-4, ...) read consecutive 8-byte words (no bank conflict)
             const int rp = (r == 0) ? Pd - 1 : r - 1;
             const float b = (rp < N) ? xq[rp] : 0.0f;
-            reinterpret_cast<float2*>(xs)[r] = make_float2(a, b);
+            reinterpret_cast<float2*>(xs)[xpair_index(r, Pd)] = make_float2(a, b);
         } else {
             xs[r] = a;
         }
@@ -279,6 +428,10 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
         bnd[r] = e;
     }
     if (threadIdx.x < 32) {
+        E e;
+        e.d = INFINITY;
+        if constexpr (TRACE) e.s = 0;
+        infs[threadIdx.x] = e;
         pp[threadIdx.x] = 0;
         const int g = rank * GW + threadIdx.x;   // successor of local warp threadIdx.x starts at 32C(g+1)
         cp[threadIdx.x] = 32 * C * (g + 1);
@@ -304,49 +457,97 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     int* pred_cp = nullptr;                                   // where we report consumption
     if (gw > 0) pred_cp = (warp > 0) ? cp + warp - 1 : cluster.map_shared_rank(cp + GW - 1, rank - 1);
     const E* my_in = (gw == 0) ? bnd : ring + warp * RS;
+    const int u_min = 32 * C * gw;                 // virtual lane of lane 0, chain 0
+    const int u_max = u_min + 32 * C - 1;          // virtual lane of lane 31, last chain
     const int u0 = C * (32 * gw + lane);
     const int u_last = V - 1;
     const int Mtot_bands = P.Pr * Pd;
 
-    // ---- per-lane state
-    Strip<C, WC> st;
-    int S[TRACE ? C : 1][TRACE ? WC : 1];
+    // ---- per-lane state (the strip's row in a rotating register file)
+    RowT R;
+    Ys<C, WC> Y;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        if constexpr (C == 1) R.D[k] = INFINITY;
+        else R.D[k] = pk(INFINITY, INFINITY);
+        if constexpr (TRACE) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) R.S[c][k] = 0;
+        }
+    }
 #pragma unroll
     for (int c = 0; c < C; ++c)
 #pragma unroll
-        for (int w = 0; w < WC; ++w) {
-            st.set_d(c, w, INFINITY);
-            st.set_y(c, w, INFINITY);
-            if constexpr (TRACE) S[c][w] = 0;
-        }
-    float prevleft[C];
-    int prevleft_s[C];
+        for (int w = 0; w < WC; ++w) Y.set(c, w, INFINITY);
+    LaneScalars<C> ls;
+#pragma unroll
+    for (int c = 0; c < C; ++c) { ls.prevleft[c] = INFINITY; ls.prevleft_s[c] = 0; }
+    ls.right0 = INFINITY; ls.right0_s = 0; ls.outv = INFINITY; ls.outs = 0;
     float best[C];
     int bestcol[C], beststart[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-        prevleft[c] = INFINITY; prevleft_s[c] = 0;
-        best[c] = INFINITY; bestcol[c] = 0x7fffffff; beststart[c] = 0;
-    }
-    float outv = INFINITY;    // right edge of the lane's last chain (to lane+1 / next warp)
-    int outs = 0;
-    float right0 = INFINITY;  // C == 2: chain 0 right edge -> chain 1 left at the next step
-    int right0_s = 0;
+    for (int c = 0; c < C; ++c) { best[c] = INFINITY; bestcol[c] = 0x7fffffff; beststart[c] = 0; }
 
-    // band of chain 0 at this warp's first step t = 32*C*gw
+    // band of chain 0 at this warp's first step t = u_min
     int b0 = -C * lane;
     int p0 = (b0 < 0) ? -1 : 0;
     int r0 = (b0 < 0) ? b0 + Pd : 0;
 
     // warp g runs steps [32*C*g, 32*C*g + span): its lanes' bands cover [0, Pr*Pd)
     const int span = (32 * C - 1 + Mtot_bands + K - 1) / K * K;
-    const int t_begin = 32 * C * gw;
+    const int t_begin = u_min;
     const int t_end = t_begin + span;
     // a predecessor never publishes past its own end: the successor's trailing
     // (idle-band) chunks must not wait for more
     const int pred_end = t_end - 32 * C;                 // = t_end of warp gw-1
     const int last_end = 32 * C * (G - 1) + span;        // = t_end of warp G-1
     const unsigned FULL = 0xffffffffu;
+
+    // One step on the slow path: per-lane round transitions / last-row folds may occur.
+    auto slow_step = [&](int t) {
+        float lin = __shfl_up_sync(FULL, ls.outv, 1);
+        int lins = 0;
+        if constexpr (TRACE) lins = __shfl_up_sync(FULL, ls.outs, 1);
+        if (lane == 0) {
+            E e;
+            if (gw == 0) {
+                if (p0 >= 1) e = my_in[r0];
+                else { e.d = INFINITY; if constexpr (TRACE) e.s = 0; }
+            } else {
+                e = my_in[(t - 1) & (RS - 1)];
+            }
+            lin = e.d;
+            if constexpr (TRACE) lins = e.s;
+        }
+        const int r1 = (r0 == 0) ? Pd - 1 : r0 - 1;   // chain 1 row
+        const int p1 = (r0 == 0) ? p0 - 1 : p0;       // chain 1 round
+        if (r0 == 0) enter_strip<C, WC, TRACE>(R, Y, 0, (long)p0 * V + u0, p0 < P.Pr, P.Y, P.Malloc, ls);
+        if (C == 2 && r1 == 0)
+            enter_strip<C, WC, TRACE>(R, Y, C - 1, (long)p1 * V + u0 + 1, p1 < P.Pr, P.Y, P.Malloc, ls);
+        unsigned long long xx;
+        if constexpr (C == 2) xx = reinterpret_cast<const unsigned long long*>(xs)[xpair_index(r0, Pd)];
+        else xx = __float_as_uint(xs[r0]);
+        row_cells<C, WC, FMA, TRACE, 0>(R, Y, xx, lin, lins, ls);
+        unrotate1<C, WC, TRACE>(R);
+        if (r0 == N - 1 && p0 >= 0 && p0 < P.Pr)
+            fold_last_row<C, WC, TRACE>(R, 0, (int)(((long)p0 * V + u0) * WC), best[0], bestcol[0], beststart[0]);
+        if (C == 2 && r1 == N - 1 && p1 >= 0 && p1 < P.Pr)
+            fold_last_row<C, WC, TRACE>(R, C - 1, (int)(((long)p1 * V + u0 + 1) * WC), best[C - 1],
+                                        bestcol[C - 1], beststart[C - 1]);
+        if (lane == 31) {
+            E e;
+            e.d = ls.outv;
+            if constexpr (TRACE) e.s = ls.outs;
+            if (has_succ_ring) {
+                succ_ring[t & (RS - 1)] = e;
+            } else {
+                const int bl = b0 - (C - 1);               // band of the last chain
+                if (bl >= 0 && bl < Mtot_bands) succ_ring[(C == 2) ? r1 : r0] = e;
+            }
+        }
+        ++b0;
+        if (++r0 == Pd) { r0 = 0; ++p0; }
+    };
 
     for (int t0 = t_begin; t0 < t_end; t0 += K) {
         // ---- chunk-level flow control (one lane each), then converge
@@ -357,116 +558,67 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
         if (lane == 31 && has_succ_ring) spin_until_geq(cp + warp, t0 + K - RS + 1, 3);
         __syncwarp();
 
+        // ---- fast chunk: no lane of this warp crosses row 0 (round transition) or
+        // row N-1 (last-row fold) -> warp-uniform, branch-free steps
+        const int blo = t0 - u_max, blen = K + 32 * C - 1;
+        const bool fast = !hits_row(blo, blen, 0, Pd) && !hits_row(blo, blen, N - 1, Pd);
+        if (fast) {
+            // Warp-uniform ring addressing, one base pointer per rotation period:
+            // lane 0 reads its left input for step t from slot t-1 of its inbox (or
+            // row t-u_min of the boundary ring for warp 0; +inf entries in round 0),
+            // lane 31 writes its right edge of step t to slot t of the successor's
+            // inbox (or row t-u_max of the boundary ring).  t0 and the period start
+            // are multiples of U, and U divides RS, so only the first read of a
+            // period can wrap around the inbox.
+            const int in_row = fmod_pos(t0 - u_min, Pd);
+            const bool lane0_inf = (gw == 0) && (t0 < Pd);
+            const int out_row = fmod_pos(t0 - u_max, Pd);
+            const unsigned long long* xpe = reinterpret_cast<const unsigned long long*>(xs) + xpair_index(r0, Pd);
+            const unsigned long long* xpo = reinterpret_cast<const unsigned long long*>(xs) + xpair_index(r0 + 1, Pd);
+            const float* x1 = xs + r0;
 #pragma unroll 1
-        for (int s = 0; s < K; ++s) {
-            const int t = t0 + s;
-            // ---- left input of chain 0: previous lane's last chain (SHFL.UP), lane 0: inbox
-            float lin = __shfl_up_sync(FULL, outv, 1);
-            int lins = 0;
-            if constexpr (TRACE) lins = __shfl_up_sync(FULL, outs, 1);
-            if (lane == 0) {
-                E e;
+            for (int s = 0; s < K; s += U) {
+                const int tg = t0 + s;
+                const E* ib0;
+                const E* ib1;
                 if (gw == 0) {
-                    if (p0 >= 1) e = my_in[r0];
-                    else { e.d = INFINITY; if constexpr (TRACE) e.s = 0; }
+                    ib0 = lane0_inf ? infs : bnd + in_row + s;
+                    ib1 = ib0 + 1;
                 } else {
-                    e = my_in[t & (RS - 1)];
+                    ib0 = my_in + ((tg - 1) & (RS - 1));
+                    ib1 = my_in + (tg & (RS - 1));
                 }
-                lin = e.d;
-                if constexpr (TRACE) lins = e.s;
-            }
-            const int r1 = (r0 == 0) ? Pd - 1 : r0 - 1;   // chain 1 row
-            const int p1 = (r0 == 0) ? p0 - 1 : p0;       // chain 1 round
-
-            // ---- round transitions (new strip: virtual row -1 = 0, reload y)
-            if (r0 == 0) {
-                const long strip = (long)p0 * V + u0;
-                enter_strip<C, WC, TRACE>(st, S, 0, strip, p0 < P.Pr, P, prevleft[0], prevleft_s[0]);
-            }
-            if (C == 2 && r1 == 0) {
-                const long strip = (long)p1 * V + u0 + 1;
-                enter_strip<C, WC, TRACE>(st, S, C - 1, strip, p1 < P.Pr, P, prevleft[C - 1], prevleft_s[C - 1]);
-            }
-
-            // ---- the cells (Eq. 1)
-            if constexpr (C == 1) {
-                const float xv = xs[r0];
-                float left = lin, diag = prevleft[0];
-                int sl = lins, sd = prevleft_s[0];
-                prevleft[0] = lin;
-                prevleft_s[0] = lins;
-#pragma unroll
-                for (int w = 0; w < WC; ++w) {
-                    const float up = st.D[w];
-                    const float m = min3f(diag, up, left);
-                    const float v = cell1<FMA>(xv, st.Y[w], m);
-                    if constexpr (TRACE) {
-                        const int su = S[0][w];
-                        const int sv = (diag == m) ? sd : ((up == m) ? su : sl);
-                        sd = su; S[0][w] = sv; sl = sv;
+                E* ob = has_succ_ring ? succ_ring + (tg & (RS - 1)) : succ_ring + out_row + s;
+                static_for<0, U>([&](auto hc) {
+                    constexpr int h = decltype(hc)::value;
+                    float lin = __shfl_up_sync(FULL, ls.outv, 1);
+                    int lins = 0;
+                    if constexpr (TRACE) lins = __shfl_up_sync(FULL, ls.outs, 1);
+                    const E e = (h == 0) ? ib0[0] : ib1[h - 1];
+                    if (lane == 0) {
+                        lin = e.d;
+                        if constexpr (TRACE) lins = e.s;
                     }
-                    diag = up; st.D[w] = v; left = v;
-                }
-                outv = left;
-                outs = sl;
-            } else {
-                const unsigned long long xx = reinterpret_cast<const unsigned long long*>(xs)[r0];
-                float l0 = lin, l1 = right0;
-                float d0 = prevleft[0], d1 = prevleft[1];
-                int sl0 = lins, sl1 = right0_s, sd0 = prevleft_s[0], sd1 = prevleft_s[1];
-                prevleft[0] = l0; prevleft[1] = l1;
-                prevleft_s[0] = sl0; prevleft_s[1] = sl1;
-#pragma unroll
-                for (int w = 0; w < WC; ++w) {
-                    const float u0v = lo32(st.D[w]), u1v = hi32(st.D[w]);
-                    const float m0 = min3f(d0, u0v, l0);
-                    const float m1 = min3f(d1, u1v, l1);
-                    unsigned long long tt, vv;
-                    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(xx), "l"(st.Y[w]));
-                    if (FMA) {
-                        asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(vv) : "l"(tt), "l"(pk(m0, m1)));
-                    } else {
-                        const float t0v = lo32(tt), t1v = hi32(tt);
-                        vv = pk(__fadd_rn(__fmul_rn(t0v, t0v), m0), __fadd_rn(__fmul_rn(t1v, t1v), m1));
+                    unsigned long long xx;
+                    if constexpr (C == 2) xx = (h & 1) ? xpo[h >> 1] : xpe[h >> 1];
+                    else xx = __float_as_uint(x1[h]);
+                    row_cells<C, WC, FMA, TRACE, h>(R, Y, xx, lin, lins, ls);
+                    if (lane == 31) {
+                        E o;
+                        o.d = ls.outv;
+                        if constexpr (TRACE) o.s = ls.outs;
+                        ob[h] = o;
                     }
-                    if constexpr (TRACE) {
-                        const int su0 = S[0][w], su1 = S[1][w];
-                        const int sv0 = (d0 == m0) ? sd0 : ((u0v == m0) ? su0 : sl0);
-                        const int sv1 = (d1 == m1) ? sd1 : ((u1v == m1) ? su1 : sl1);
-                        sd0 = su0; sd1 = su1; S[0][w] = sv0; S[1][w] = sv1; sl0 = sv0; sl1 = sv1;
-                    }
-                    st.D[w] = vv;
-                    d0 = u0v; d1 = u1v;
-                    l0 = lo32(vv); l1 = hi32(vv);
-                }
-                right0 = l0; right0_s = sl0;
-                outv = l1; outs = sl1;
+                });
+                if constexpr (C == 2) { xpe += U / 2; xpo += U / 2; }
+                else x1 += U;
             }
-
-            // ---- last-row fold (minimum extracted as the bottom row is produced)
-            if (r0 == N - 1 && p0 >= 0 && p0 < P.Pr)
-                fold_last_row<C, WC, TRACE>(st, S, 0, (int)(((long)p0 * V + u0) * WC), best[0], bestcol[0],
-                                            beststart[0]);
-            if (C == 2 && r1 == N - 1 && p1 >= 0 && p1 < P.Pr)
-                fold_last_row<C, WC, TRACE>(st, S, C - 1, (int)(((long)p1 * V + u0 + 1) * WC), best[C - 1],
-                                            bestcol[C - 1], beststart[C - 1]);
-
-            // ---- lane 31: right edge to the next warp's inbox (or the boundary ring)
-            if (lane == 31) {
-                E e;
-                e.d = outv;
-                if constexpr (TRACE) e.s = outs;
-                if (has_succ_ring) {
-                    succ_ring[(t + 1) & (RS - 1)] = e;
-                } else {
-                    const int bl = b0 - (C - 1);               // band of the last chain
-                    if (bl >= 0 && bl < Mtot_bands) succ_ring[(C == 2) ? r1 : r0] = e;
-                }
-            }
-
-            // ---- advance
-            ++b0;
-            if (++r0 == Pd) { r0 = 0; ++p0; }
+            b0 += K;
+            r0 += K;                                     // may land exactly on the next round
+            if (r0 >= Pd) { r0 -= Pd; ++p0; }
+        } else {
+#pragma unroll 1
+            for (int s = 0; s < K; ++s) slow_step(t0 + s);
         }
 
         // ---- publish progress

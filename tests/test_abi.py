@@ -58,8 +58,8 @@ def test_version_and_options(lib):
     assert e.value.status == sd.E_ARG
     with pytest.raises(sd.SdtwError):
         sd.set_option(sd.OPT_NORMALIZE, 7)
-    with sd.options(OPT_SEGMENT_W=16):
-        assert sd.get_option(sd.OPT_SEGMENT_W) == 16
+    with sd.options(OPT_SEGMENT_W=14):
+        assert sd.get_option(sd.OPT_SEGMENT_W) == 14
     assert sd.get_option(sd.OPT_SEGMENT_W) == 0
 
 

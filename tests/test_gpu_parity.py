@@ -67,16 +67,17 @@ def _check_exact(Q, Y, got, fma=True, trace=False, ref=None):
 # --------------------------------------------------------------- bit-exact DP
 SCHEDULES = [
     dict(),                                                  # auto
-    dict(OPT_PACKED=0, OPT_SEGMENT_W=8, OPT_LANES=1),
-    dict(OPT_PACKED=0, OPT_SEGMENT_W=16, OPT_LANES=2, OPT_CHUNK=16),
-    dict(OPT_PACKED=0, OPT_SEGMENT_W=32, OPT_LANES=4),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=8, OPT_LANES=1, OPT_CHUNK=8),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=16, OPT_LANES=3),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=24, OPT_LANES=2, OPT_CLUSTER=2),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=32, OPT_LANES=4, OPT_CLUSTER=2),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=48, OPT_LANES=1, OPT_CLUSTER=4),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=64, OPT_LANES=2),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=32, OPT_LANES=1, OPT_CLUSTER=8, OPT_CHUNK=16),
+    dict(OPT_PACKED=0, OPT_SEGMENT_W=7, OPT_LANES=1),
+    dict(OPT_PACKED=0, OPT_SEGMENT_W=15, OPT_LANES=2, OPT_CHUNK=16),
+    dict(OPT_PACKED=0, OPT_SEGMENT_W=31, OPT_LANES=4),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=6, OPT_LANES=1, OPT_CHUNK=8),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=14, OPT_LANES=3),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=14, OPT_LANES=2, OPT_CLUSTER=2),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=30, OPT_LANES=4, OPT_CLUSTER=2),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=62, OPT_LANES=1, OPT_CLUSTER=4),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=62, OPT_LANES=2),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=30, OPT_LANES=1, OPT_CLUSTER=8, OPT_CHUNK=16),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=6, OPT_LANES=8, OPT_CHUNK=64),
 ]
 
 
