@@ -55,7 +55,8 @@ enum {
     SDTW_OPT_PACKED = 7,    /* 1: two chains per lane with f32x2 FADD2/FFMA2; 0: scalar;
                                -1 (default) = auto */
     SDTW_OPT_CHUNK = 8,     /* steps between inter-warp handoff checks (8,16,32); 0 = auto */
-    SDTW_OPT_PROFILE = 9    /* 1: time the DP kernel with CUDA events (sdtw_profile) */
+    SDTW_OPT_PROFILE = 9,   /* 1: time the DP kernel with CUDA events (sdtw_profile) */
+    SDTW_OPT_RING = 10      /* inter-warp hand-off ring entries (rounded up to a power of two); 0 = auto */
 };
 
 /* Install the reference Y[M] on the current device (copied into a

@@ -28,6 +28,7 @@ struct Options {
     int packed = -1;
     int chunk = 0;
     int profile = 0;
+    int ring = 0;
     cudaStream_t stream = 0;
 };
 Options g_opt;
@@ -118,26 +119,30 @@ int ptr_kind(const void* p) {
 using sdtw::DpParams;
 typedef void (*DpKernel)(DpParams);
 
+template <int C, int WC, bool FMA, bool TRACE>
+DpKernel pick_cluster(bool cl) {
+    return cl ? sdtw::sdtw_dp_kernel<C, WC, FMA, TRACE, true> : sdtw::sdtw_dp_kernel<C, WC, FMA, TRACE, false>;
+}
 template <int C, int WC>
-DpKernel pick_fma_trace(bool fma, bool trace) {
-    if (fma) return trace ? sdtw::sdtw_dp_kernel<C, WC, true, true> : sdtw::sdtw_dp_kernel<C, WC, true, false>;
-    return trace ? sdtw::sdtw_dp_kernel<C, WC, false, true> : sdtw::sdtw_dp_kernel<C, WC, false, false>;
+DpKernel pick_fma_trace(bool fma, bool trace, bool cl) {
+    if (fma) return trace ? pick_cluster<C, WC, true, true>(cl) : pick_cluster<C, WC, true, false>(cl);
+    return trace ? pick_cluster<C, WC, false, true>(cl) : pick_cluster<C, WC, false, false>(cl);
 }
 
-DpKernel pick_kernel(int C, int WC, bool fma, bool trace) {
+DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl) {
     if (C == 1) {
         switch (WC) {
-            case 7: return pick_fma_trace<1, 7>(fma, trace);
-            case 15: return pick_fma_trace<1, 15>(fma, trace);
-            case 31: return pick_fma_trace<1, 31>(fma, trace);
+            case 7: return pick_fma_trace<1, 7>(fma, trace, cl);
+            case 15: return pick_fma_trace<1, 15>(fma, trace, cl);
+            case 31: return pick_fma_trace<1, 31>(fma, trace, cl);
             default: return nullptr;
         }
     }
     switch (WC) {
-        case 3: return pick_fma_trace<2, 3>(fma, trace);
-        case 7: return pick_fma_trace<2, 7>(fma, trace);
-        case 15: return pick_fma_trace<2, 15>(fma, trace);
-        case 31: return pick_fma_trace<2, 31>(fma, trace);
+        case 3: return pick_fma_trace<2, 3>(fma, trace, cl);
+        case 7: return pick_fma_trace<2, 7>(fma, trace, cl);
+        case 15: return pick_fma_trace<2, 15>(fma, trace, cl);
+        case 31: return pick_fma_trace<2, 31>(fma, trace, cl);
         default: return nullptr;
     }
 }
@@ -152,7 +157,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     int W = o.segment_w > 0 ? o.segment_w : (C == 2 ? 30 : 31);
     if (W % C != 0) return fail(SDTW_E_ARG, "segment width must be a multiple of the chains per lane");
     int WC = W / C;
-    if (!pick_kernel(C, WC, true, false))
+    if (!pick_kernel(C, WC, true, false, false))
         return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) +
                                     (C == 2 ? " (packed: 6,14,30,62)" : " (scalar: 7,15,31)"));
     int GW = o.lanes > 0 ? o.lanes : 4;
@@ -169,8 +174,11 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     const int64_t Pr = (ctx.M + V * WC - 1) / (V * WC);
     if (Pr * Pd + V + 2 * K >= (1LL << 31) || Pr * V * WC >= (1LL << 31))
         return fail(SDTW_E_ARG, "problem too large for 32-bit step/column counters");
+    // inter-warp ring depth: deep enough to absorb one warp's round-transition
+    // (slow) chunks without stalling its neighbours
     int RS = 1;
-    while (RS < 4 * K) RS <<= 1;
+    const int RSmin = std::max(4 * K, o.ring > 0 ? (int)o.ring : 1024);
+    while (RS < RSmin) RS <<= 1;
     const sdtw::SmemLayout L = sdtw::smem_layout(C, trace, GW, CL, (int)Pd, RS);
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
     *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes};
@@ -179,7 +187,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
 }
 
 sdtw_status launch_dp(const LaunchCfg& c, bool fma, bool trace, const DpParams& p, cudaStream_t st) {
-    DpKernel k = pick_kernel(c.C, c.WC, fma, trace);
+    DpKernel k = pick_kernel(c.C, c.WC, fma, trace, c.CL > 1);
     CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem));
     if (c.CL > 8) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t lc;
@@ -407,6 +415,7 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_PACKED: if (v < -1 || v > 1) break; g_opt.packed = (int)v; return SDTW_OK;
         case SDTW_OPT_CHUNK: if (v < 0 || v > 256) break; g_opt.chunk = (int)v; return SDTW_OK;
         case SDTW_OPT_PROFILE: if (v != 0 && v != 1) break; g_opt.profile = (int)v; return SDTW_OK;
+        case SDTW_OPT_RING: if (v < 0 || v > 16384) break; g_opt.ring = (int)v; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
     return fail(SDTW_E_ARG, "bad value for option " + std::to_string(key));
@@ -425,6 +434,7 @@ sdtw_status sdtw_get_option(int key, int64_t* v) {
         case SDTW_OPT_PACKED: *v = g_opt.packed; return SDTW_OK;
         case SDTW_OPT_CHUNK: *v = g_opt.chunk; return SDTW_OK;
         case SDTW_OPT_PROFILE: *v = g_opt.profile; return SDTW_OK;
+        case SDTW_OPT_RING: *v = g_opt.ring; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
 }

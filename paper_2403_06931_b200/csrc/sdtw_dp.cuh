@@ -58,29 +58,56 @@ template <> struct Entry<true> { float d; int s; };
 __device__ __forceinline__ void st_release_cluster(int* p, int v) {
     asm volatile("st.release.cluster.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v)
+                 : "memory");
+}
 __device__ __forceinline__ int ld_acquire_cluster(const int* p) {
     int v;
     asm volatile("ld.acquire.cluster.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];"
+                 : "=r"(v)
+                 : "r"((unsigned)__cvta_generic_to_shared(p))
+                 : "memory");
+    return v;
+}
+// Progress counters live in the waiting warp's own CTA.  When the whole ring is
+// one CTA (no cluster) every hand-off is CTA-scoped: an LDS-class acquire, no
+// L1 invalidation.  Across cluster CTAs the acquire must be cluster-scoped.
+template <bool CLUSTER>
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    return CLUSTER ? ld_acquire_cluster(p) : ld_acquire_cta(p);
+}
+template <bool CLUSTER>
+__device__ __forceinline__ void st_release(int* p, int v, bool local) {
+    if (CLUSTER && !local) st_release_cluster(p, v);
+    else if (CLUSTER) st_release_cluster(p, v);
+    else st_release_cta(p, v);
+}
 // Wait until *p >= need.  A watchdog turns a protocol bug into a diagnosable trap
 // instead of a hung GPU (never reached in a correct run: every wait is bounded by
 // the ring's progress).
+template <bool CLUSTER>
 __device__ __noinline__ void spin_slow(const int* p, int need, int tag) {
     long long n = 0;
     int v;
-    while ((v = ld_acquire_cluster(p)) < need) {
-        __nanosleep(32);
-        if (++n == (1LL << 25)) {
+    while ((v = ld_acquire<CLUSTER>(p)) < need) {
+        __nanosleep(128);
+        if (++n == (1LL << 24)) {
             printf("sdtw watchdog: block %d thread %d tag %d waits *p=%d >= %d\n", (int)blockIdx.x,
                    (int)threadIdx.x, tag, v, need);
             __trap();
         }
     }
 }
+template <bool CLUSTER>
 __device__ __forceinline__ void spin_until_geq(const int* p, int need, int tag = 0) {
-    if (ld_acquire_cluster(p) >= need) return;
-    spin_slow(p, need, tag);
+    if (ld_acquire<CLUSTER>(p) >= need) return;
+    spin_slow<CLUSTER>(p, need, tag);
 }
 
 __device__ __forceinline__ unsigned long long pk2(float2 a) {
@@ -378,7 +405,7 @@ __device__ __forceinline__ bool hits_row(int blo, int len, int row, int Pd) {
     return fmod_pos(row - blo, Pd) < len;
 }
 
-template <int C, int WC, bool FMA, bool TRACE>
+template <int C, int WC, bool FMA, bool TRACE, bool CLUSTER>
 __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     static_assert(C == 1 || C == 2, "C");
     static_assert(((WC + 1) & WC) == 0 && (32 * C) % (WC + 1) == 0,
@@ -552,10 +579,10 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     for (int t0 = t_begin; t0 < t_end; t0 += K) {
         // ---- chunk-level flow control (one lane each), then converge
         if (lane == 0) {
-            if (gw > 0) spin_until_geq(pp + warp, min(t0 + K - 1, pred_end), 1);
-            else if (t0 + K - 1 >= Pd) spin_until_geq(pp, min(t0 + K - Pd + u_last, last_end), 2);
+            if (gw > 0) spin_until_geq<CLUSTER>(pp + warp, min(t0 + K - 1, pred_end), 1);
+            else if (t0 + K - 1 >= Pd) spin_until_geq<CLUSTER>(pp, min(t0 + K - Pd + u_last, last_end), 2);
         }
-        if (lane == 31 && has_succ_ring) spin_until_geq(cp + warp, t0 + K - RS + 1, 3);
+        if (lane == 31 && has_succ_ring) spin_until_geq<CLUSTER>(cp + warp, t0 + K - RS + 1, 3);
         __syncwarp();
 
         // ---- fast chunk: no lane of this warp crosses row 0 (round transition) or
@@ -623,8 +650,8 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
 
         // ---- publish progress
         __syncwarp();
-        if (lane == 31) st_release_cluster(succ_pp, t0 + K);
-        if (lane == 0 && gw > 0) st_release_cluster(pred_cp, t0 + K);
+        if (lane == 31) st_release<CLUSTER>(succ_pp, t0 + K, true);
+        if (lane == 0 && gw > 0) st_release<CLUSTER>(pred_cp, t0 + K, true);
     }
 
     // ---- reduction of (cost, col[, start]) over chains, lanes, warps, cluster CTAs
