@@ -48,13 +48,15 @@ enum {
     SDTW_OPT_FMA = 2,       /* 1 (default): cell = fmaf(t,t,m); 0: fl(fl(t*t)+m) -- both
                                bit-exact with the oracle in the same mode */
     SDTW_OPT_SEGMENT_W = 3, /* reference columns per lane ("segment width"):
-                               packed 6, 14, 30 (default), 62; scalar 7, 15, 31; 0 = auto */
+                               scalar 7, 15, 31; 2 chains 6, 14, 30 (default), 62; 4 chains 28, 60;
+                               0 = auto */
     SDTW_OPT_LANES = 4,     /* warps per CTA in one query ring; 0 = auto */
     SDTW_OPT_CLUSTER = 5,   /* CTAs per query (thread-block cluster, DSMEM handoff); 0 = auto */
     SDTW_OPT_STREAM = 6,    /* cudaStream_t as int64 (0 = legacy default stream) */
-    SDTW_OPT_PACKED = 7,    /* 1: two chains per lane with f32x2 FADD2/FFMA2; 0: scalar;
-                               -1 (default) = auto */
-    SDTW_OPT_CHUNK = 8,     /* steps between inter-warp handoff checks (8,16,32); 0 = auto */
+    SDTW_OPT_PACKED = 7,    /* chains per lane: 0 = 1 (scalar FADD/FMNMX3/FFMA), 1 = 2 (one f32x2
+                               FADD2/FFMA2 pair), 2 = 4 (two independent pairs); -1 = auto (2) */
+    SDTW_OPT_CHUNK = 8,     /* steps between inter-warp hand-off checks, rounded to whole
+                               rotation periods (WC+1 steps); 0 = auto (32) */
     SDTW_OPT_PROFILE = 9,   /* 1: time the DP kernel with CUDA events (sdtw_profile) */
     SDTW_OPT_RING = 10      /* inter-warp hand-off ring entries (rounded up to a power of two); 0 = auto */
 };

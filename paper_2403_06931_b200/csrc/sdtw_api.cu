@@ -6,6 +6,7 @@
 // there is no CPU fallback: without a CUDA device every call returns SDTW_E_CUDA.
 #include "../../include/sdtw.h"
 #include "sdtw_dp.cuh"
+#include "sdtw_dp_pick.h"
 #include "sdtw_prep.cuh"
 
 #include <atomic>
@@ -117,32 +118,13 @@ int ptr_kind(const void* p) {
 
 // ------------------------------------------------------------------ DP dispatch
 using sdtw::DpParams;
-typedef void (*DpKernel)(DpParams);
-
-template <int C, int WC, bool FMA, bool TRACE>
-DpKernel pick_cluster(bool cl) {
-    return cl ? sdtw::sdtw_dp_kernel<C, WC, FMA, TRACE, true> : sdtw::sdtw_dp_kernel<C, WC, FMA, TRACE, false>;
-}
-template <int C, int WC>
-DpKernel pick_fma_trace(bool fma, bool trace, bool cl) {
-    if (fma) return trace ? pick_cluster<C, WC, true, true>(cl) : pick_cluster<C, WC, true, false>(cl);
-    return trace ? pick_cluster<C, WC, false, true>(cl) : pick_cluster<C, WC, false, false>(cl);
-}
+using sdtw::DpKernel;
 
 DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl) {
-    if (C == 1) {
-        switch (WC) {
-            case 7: return pick_fma_trace<1, 7>(fma, trace, cl);
-            case 15: return pick_fma_trace<1, 15>(fma, trace, cl);
-            case 31: return pick_fma_trace<1, 31>(fma, trace, cl);
-            default: return nullptr;
-        }
-    }
-    switch (WC) {
-        case 3: return pick_fma_trace<2, 3>(fma, trace, cl);
-        case 7: return pick_fma_trace<2, 7>(fma, trace, cl);
-        case 15: return pick_fma_trace<2, 15>(fma, trace, cl);
-        case 31: return pick_fma_trace<2, 31>(fma, trace, cl);
+    switch (C) {
+        case 1: return sdtw::pick_dp_c1(WC, fma, trace, cl);
+        case 2: return sdtw::pick_dp_c2(WC, fma, trace, cl);
+        case 4: return sdtw::pick_dp_c4(WC, fma, trace, cl);
         default: return nullptr;
     }
 }
@@ -153,13 +135,14 @@ struct LaunchCfg {
 
 sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cfg) {
     const Options& o = g_opt;
-    int C = (o.packed < 0) ? 2 : (o.packed ? 2 : 1);
-    int W = o.segment_w > 0 ? o.segment_w : (C == 2 ? 30 : 31);
+    // chains per lane: 1 scalar, 2 = one f32x2 pair, 4 = two independent pairs
+    int C = (o.packed < 0) ? 2 : (o.packed == 0 ? 1 : (o.packed == 1 ? 2 : 4));
+    int W = o.segment_w > 0 ? o.segment_w : (C == 4 ? 28 : (C == 2 ? 30 : 31));
     if (W % C != 0) return fail(SDTW_E_ARG, "segment width must be a multiple of the chains per lane");
     int WC = W / C;
     if (!pick_kernel(C, WC, true, false, false))
         return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) +
-                                    (C == 2 ? " (packed: 6,14,30,62)" : " (scalar: 7,15,31)"));
+                                    (C == 4 ? " (4 chains: 28,60)" : C == 2 ? " (packed: 6,14,30,62)" : " (scalar: 7,15,31)"));
     int GW = o.lanes > 0 ? o.lanes : 4;
     int CL = o.cluster > 0 ? o.cluster : 1;
     if (GW < 1 || GW > 8 || CL < 1 || CL > 16) return fail(SDTW_E_ARG, "lanes (1..8) / cluster (1..16) out of range");
@@ -179,7 +162,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     int RS = 1;
     const int RSmin = std::max(4 * K, o.ring > 0 ? (int)o.ring : 1024);
     while (RS < RSmin) RS <<= 1;
-    const sdtw::SmemLayout L = sdtw::smem_layout(C, trace, GW, CL, (int)Pd, RS);
+    const sdtw::SmemLayout L = sdtw::smem_layout(C, trace, GW, (int)Pd, RS);
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
     *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes};
     (void)Z;
@@ -412,7 +395,7 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_LANES: if (v < 0 || v > 16) break; g_opt.lanes = (int)v; return SDTW_OK;
         case SDTW_OPT_CLUSTER: if (v < 0 || v > 16) break; g_opt.cluster = (int)v; return SDTW_OK;
         case SDTW_OPT_STREAM: g_opt.stream = reinterpret_cast<cudaStream_t>(v); return SDTW_OK;
-        case SDTW_OPT_PACKED: if (v < -1 || v > 1) break; g_opt.packed = (int)v; return SDTW_OK;
+        case SDTW_OPT_PACKED: if (v < -1 || v > 2) break; g_opt.packed = (int)v; return SDTW_OK;
         case SDTW_OPT_CHUNK: if (v < 0 || v > 256) break; g_opt.chunk = (int)v; return SDTW_OK;
         case SDTW_OPT_PROFILE: if (v != 0 && v != 1) break; g_opt.profile = (int)v; return SDTW_OK;
         case SDTW_OPT_RING: if (v < 0 || v > 16384) break; g_opt.ring = (int)v; return SDTW_OK;

@@ -14,25 +14,30 @@
 //  * Virtual lane u processes band b = t-u at global step t (row r = b mod Pd of
 //    round p = b div Pd; Pd >= N is the round period, rows >= N are idle).  So
 //    each step is one anti-diagonal of virtual lanes.
-//  * Strip state lives in registers: D[w] holds the previous row of the strip and
-//    is updated in place with a rolling diag (the paper's two row buffers).
-//  * Right-edge hand-off: chain c -> chain c+1 in the same lane is a register; the
+//  * Strip state lives in registers (the paper's two row buffers of segment width,
+//    P:L100, become one ROTATING register file of WC+1 slots, see RotRow).
+//  * Right-edge hand-off: chain c -> chain c+1 of the same lane is a register; the
 //    last chain -> next lane by SHFL.UP ("__shfl_up"); lane 31 -> next warp
 //    through a shared-memory ring (DSMEM when the next warp is in another CTA of
 //    the cluster) with release/acquire progress counters checked every K steps;
 //    the last virtual lane -> virtual lane 0 of the next round through the
 //    Pd-entry boundary ring (the paper's "shared memory buffer which represents the
 //    last segment values").
-//  * C == 2 packs the two chains of a lane into f32x2 FADD2/FFMA2 (sm_100a):
-//    per 2 cells FADD2 + FFMA2 + 2 FMNMX3 = 2 SASS/cell instead of 3.
+//  * C >= 2 packs chains (2p, 2p+1) into f32x2 FADD2/FFMA2 (sm_100a): per 2 cells
+//    FADD2 + FFMA2 + 2 FMNMX3 = 2 SASS/cell instead of 3; C == 4 runs two such
+//    independent pairs per lane (ILP 2 on the FMNMX3 -> FFMA2 dependency chain).
+//  * Steps are grouped in chunks of K; a chunk in which no lane of the warp crosses
+//    a round boundary (row 0) or the last row (row N-1) is "fast": branch-free,
+//    warp-uniform addressing, unrolled one rotation period at a time.  The few
+//    other chunks take the per-lane "slow" path (round transition, last-row fold).
 //  * TRACE carries, per cell, the start column of its argmin predecessor
 //    (priority diag > up > left on equality; reading G6).
 #pragma once
 #include <cooperative_groups.h>
-#include <cstdio>
 #include <cstdint>
-#include <type_traits>
+#include <cstdio>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 namespace sdtw {
 namespace cg = cooperative_groups;
@@ -40,12 +45,12 @@ namespace cg = cooperative_groups;
 struct DpParams {
     const float* X;        // [Z][N] query samples (normalised or raw), device
     const float* Y;        // reference, device, Malloc floats (+inf beyond M)
-    int Malloc;            // padded reference length (multiple of 4)
+    int Malloc;            // padded reference length
     int Z, N, M;
     int Pd;                // round period in steps (>= N)
     int Pr;                // number of rounds
-    int K;                 // steps per hand-off chunk (divides 32*C)
-    int RS;                // inter-warp ring entries (power of two, >= 4K)
+    int K;                 // steps per hand-off chunk (multiple of WC+1)
+    int RS;                // inter-warp ring entries (power of two, multiple of WC+1)
     float* out_cost;
     int64_t* out_end;
     int64_t* out_start;    // TRACE only
@@ -55,6 +60,7 @@ struct DpParams {
 template <bool TRACE> struct Entry { float d; };
 template <> struct Entry<true> { float d; int s; };
 
+// ------------------------------------------------------------ synchronisation
 __device__ __forceinline__ void st_release_cluster(int* p, int v) {
     asm volatile("st.release.cluster.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -76,16 +82,16 @@ __device__ __forceinline__ int ld_acquire_cta(const int* p) {
     return v;
 }
 // Progress counters live in the waiting warp's own CTA.  When the whole ring is
-// one CTA (no cluster) every hand-off is CTA-scoped: an LDS-class acquire, no
-// L1 invalidation.  Across cluster CTAs the acquire must be cluster-scoped.
+// one CTA (no cluster) every hand-off is CTA-scoped (an LDS-class acquire, no L1
+// invalidation); across cluster CTAs the acquire/release must be cluster-scoped.
 template <bool CLUSTER>
 __device__ __forceinline__ int ld_acquire(const int* p) {
-    return CLUSTER ? ld_acquire_cluster(p) : ld_acquire_cta(p);
+    if constexpr (CLUSTER) return ld_acquire_cluster(p);
+    else return ld_acquire_cta(p);
 }
 template <bool CLUSTER>
-__device__ __forceinline__ void st_release(int* p, int v, bool local) {
-    if (CLUSTER && !local) st_release_cluster(p, v);
-    else if (CLUSTER) st_release_cluster(p, v);
+__device__ __forceinline__ void st_release(int* p, int v) {
+    if constexpr (CLUSTER) st_release_cluster(p, v);
     else st_release_cta(p, v);
 }
 // Wait until *p >= need.  A watchdog turns a protocol bug into a diagnosable trap
@@ -105,76 +111,12 @@ __device__ __noinline__ void spin_slow(const int* p, int need, int tag) {
     }
 }
 template <bool CLUSTER>
-__device__ __forceinline__ void spin_until_geq(const int* p, int need, int tag = 0) {
+__device__ __forceinline__ void spin_until_geq(const int* p, int need, int tag) {
     if (ld_acquire<CLUSTER>(p) >= need) return;
     spin_slow<CLUSTER>(p, need, tag);
 }
 
-__device__ __forceinline__ unsigned long long pk2(float2 a) {
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
-    return r;
-}
-__device__ __forceinline__ float2 upk2(unsigned long long r) {
-    float2 a;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
-    return a;
-}
-// t = a - b, two lanes, one FADD2 (round-to-nearest, same as two scalar FADD)
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
-    unsigned long long r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
-    return upk2(r);
-}
-// a*b + c, two lanes, one FFMA2 (single rounding each, same as fmaf)
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-    unsigned long long r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
-    return upk2(r);
-}
-
-__device__ __forceinline__ float min3f(float a, float b, float c) { return fminf(fminf(a, b), c); }
-
-// fp32 cell value d(x,y) + m (the oracle's `cell`, scalar)
-template <bool FMA>
-__device__ __forceinline__ float cell1(float x, float y, float m) {
-    float t = __fsub_rn(x, y);
-    if (FMA) return __fmaf_rn(t, t, m);
-    return __fadd_rn(__fmul_rn(t, t), m);
-}
-
-// lexicographic (cost, col) "a better than b"
-__device__ __forceinline__ bool better(float ca, int ja, float cb, int jb) {
-    return ca < cb || (ca == cb && ja < jb);
-}
-
-// Shared-memory carve-up (dynamic).  Returns total bytes.
-struct SmemLayout {
-    int off_ctr, off_red, off_inf, off_x, off_bnd, off_ring, bytes;
-};
-__host__ __device__ inline SmemLayout smem_layout(int C, bool trace, int GW, int CL, int Pd, int RS) {
-    SmemLayout L;
-    const int ent = trace ? 8 : 4;
-    int o = 0;
-    L.off_ctr = o;  o += 2 * 32 * 4;                   // pp[32], cp[32]
-    L.off_red = o;  o += 16 * (32 + 16);               // per-warp + per-rank partials
-    L.off_inf = o;  o += 32 * 8;                        // +inf inbox entries (round 0)
-    o = (o + 15) & ~15;
-    L.off_x = o;    o += (Pd + 1) * C * 4;
-    o = (o + 15) & ~15;
-    L.off_bnd = o;  o += Pd * ent;
-    o = (o + 15) & ~15;
-    L.off_ring = o; o += GW * RS * ent;
-    L.bytes = (o + 15) & ~15;
-    (void)CL;
-    return L;
-}
-
-struct Partial { float cost; int col; int start; int pad; };
-
-// ----------------------------------------------------------------------------
-// Register state of one lane.  C == 2 keeps (chain0, chain1) pairs in aligned
-// 64-bit registers so that FADD2 / FFMA2 read and write them in place.
+// ------------------------------------------------------------ arithmetic
 __device__ __forceinline__ float lo32(unsigned long long r) {
     float a, b;
     asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
@@ -190,183 +132,259 @@ __device__ __forceinline__ unsigned long long pk(float a, float b) {
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
     return r;
 }
+__device__ __forceinline__ float min3f(float a, float b, float c) { return fminf(fminf(a, b), c); }
 
+// fp32 cell value d(x,y) + m (the oracle's `cell`), scalar
+template <bool FMA>
+__device__ __forceinline__ float cell1(float x, float y, float m) {
+    const float t = __fsub_rn(x, y);
+    if (FMA) return __fmaf_rn(t, t, m);
+    return __fadd_rn(__fmul_rn(t, t), m);
+}
+// the same for two chains at once: one FADD2 + one FFMA2 (each lane rounded as the scalar ops)
+template <bool FMA>
+__device__ __forceinline__ unsigned long long cell2(unsigned long long xx, unsigned long long yy, float m0,
+                                                    float m1) {
+    unsigned long long tt, vv;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(xx), "l"(yy));
+    if (FMA) {
+        asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(vv) : "l"(tt), "l"(pk(m0, m1)));
+    } else {
+        const float t0 = lo32(tt), t1 = hi32(tt);
+        vv = pk(__fadd_rn(__fmul_rn(t0, t0), m0), __fadd_rn(__fmul_rn(t1, t1), m1));
+    }
+    return vv;
+}
+
+// lexicographic (cost, col): "a better than b"
+__device__ __forceinline__ bool better(float ca, int ja, float cb, int jb) {
+    return ca < cb || (ca == cb && ja < jb);
+}
+
+// ------------------------------------------------------------ shared memory
+// Row samples: with XC = min(C, 2) floats per row, row r stores (x_r[, x_{r-1}])
+// (indices mod Pd, idle rows are 0) and rows are split by residue r mod XC, so the
+// lanes of a warp (rows r, r-C, r-2C, ...; C even => one residue class) read
+// consecutive XC-float words.  C == 4 reads the pairs of rows r and r-2.
+__host__ __device__ __forceinline__ int xrow_stride(int Pd, int XC) { return (Pd + XC - 1) / XC; }
+__host__ __device__ __forceinline__ int xrow_index(int r, int Pd, int XC) {
+    return (r % XC) * xrow_stride(Pd, XC) + r / XC;
+}
+__host__ __device__ __forceinline__ constexpr int xrow_floats(int C) { return C == 1 ? 1 : 2; }
+
+struct SmemLayout {
+    int off_ctr, off_red, off_inf, off_x, off_bnd, off_ring, bytes;
+};
+__host__ __device__ inline SmemLayout smem_layout(int C, bool trace, int GW, int Pd, int RS) {
+    SmemLayout L;
+    const int ent = trace ? 8 : 4;
+    int o = 0;
+    L.off_ctr = o;  o += 2 * 32 * 4;                    // pp[32], cp[32]
+    L.off_red = o;  o += 16 * (32 + 16);                // per-warp + per-rank partials
+    L.off_inf = o;  o += 32 * 8;                        // +inf inbox entries (round 0)
+    o = (o + 15) & ~15;
+    L.off_x = o;    o += xrow_stride(Pd, xrow_floats(C)) * xrow_floats(C) * xrow_floats(C) * 4;
+    o = (o + 15) & ~15;
+    L.off_bnd = o;  o += Pd * ent;
+    o = (o + 15) & ~15;
+    L.off_ring = o; o += GW * RS * ent;
+    L.bytes = (o + 15) & ~15;
+    return L;
+}
+
+struct Partial { float cost; int col; int start; int pad; };
+
+// ------------------------------------------------------------ register state
 // A lane's row state lives in a ROTATING register file of U = WC+1 slots per
-// chain (pairs of chains packed in 64-bit registers when C == 2): each cell's new
-// value is written into the slot of its diag input, which dies at that cell, so
-// the row moves one slot down per step and returns to its origin after U steps.
-// The fast loop is unrolled U steps so every slot index is a compile-time
-// constant and no register-to-register moves are needed.
-template <int C> struct RegT { using T = float; };
-template <> struct RegT<2> { using T = unsigned long long; };
-
+// chain (chains 2p, 2p+1 packed in one 64-bit register when C >= 2): each cell's
+// new value is written into the slot of its diag input, which dies at that cell,
+// so the row moves one slot down per step and is back at its origin after U
+// steps.  The fast loop is unrolled U steps so every slot index is a
+// compile-time constant and no register-to-register moves are needed.
 template <int C, int WC, bool TRACE> struct RotRow {
     static constexpr int U = WC + 1;
-    typename RegT<C>::T D[U];
+    static constexpr int NP = (C + 1) / 2;   // registers per slot
+    using T = typename std::conditional<C == 1, float, unsigned long long>::type;
+    T D[NP][U];
     int S[TRACE ? C : 1][TRACE ? U : 1];
-    // element w of the row when the rotation offset is h (row at slots (w - h) mod U)
     __device__ __forceinline__ static constexpr int slot(int w, int h) { return ((w - h) % U + U) % U; }
-    __device__ __forceinline__ float d(int c, int w, int h = 0) const {
-        if constexpr (C == 1) return D[slot(w, h)];
-        else return c ? hi32(D[slot(w, h)]) : lo32(D[slot(w, h)]);
+    __device__ __forceinline__ float d(int c, int w) const {   // offset 0
+        if constexpr (C == 1) return D[0][w];
+        else return (c & 1) ? hi32(D[c >> 1][w]) : lo32(D[c >> 1][w]);
     }
-    __device__ __forceinline__ void set_d(int c, int w, float v, int h = 0) {
-        if constexpr (C == 1) D[slot(w, h)] = v;
-        else {
-            const int k = slot(w, h);
-            D[k] = c ? pk(lo32(D[k]), v) : pk(v, hi32(D[k]));
+    __device__ __forceinline__ void set_all(int c, float v) {  // every slot of chain c
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            if constexpr (C == 1) D[0][k] = v;
+            else D[c >> 1][k] = (c & 1) ? pk(lo32(D[c >> 1][k]), v) : pk(v, hi32(D[c >> 1][k]));
         }
     }
-    __device__ __forceinline__ int s(int c, int w, int h = 0) const {
-        if constexpr (TRACE) return S[c][slot(w, h)];
-        else return 0;
+};
+template <int C, int WC> struct Ys {
+    static constexpr int NP = (C + 1) / 2;
+    using T = typename std::conditional<C == 1, float, unsigned long long>::type;
+    T Y[NP][WC];
+    __device__ __forceinline__ void set(int c, int w, float v) {
+        if constexpr (C == 1) Y[0][w] = v;
+        else Y[c >> 1][w] = (c & 1) ? pk(lo32(Y[c >> 1][w]), v) : pk(v, hi32(Y[c >> 1][w]));
     }
-    __device__ __forceinline__ void set_s(int c, int w, int v, int h = 0) {
-        if constexpr (TRACE) S[c][slot(w, h)] = v;
-    }
 };
-template <int C, int WC> struct Ys;
-template <int WC> struct Ys<1, WC> {
-    float Y[WC];
-    __device__ __forceinline__ void set(int, int w, float v) { Y[w] = v; }
-};
-template <int WC> struct Ys<2, WC> {
-    unsigned long long Y[WC];
-    __device__ __forceinline__ void set(int c, int w, float v) { Y[w] = c ? pk(lo32(Y[w]), v) : pk(v, hi32(Y[w])); }
-};
-
 // Per-lane scalars carried from step to step.
 template <int C> struct LaneScalars {
-    float prevleft[C];   // left input of the previous row (the next row's diag at column 0)
+    float prevleft[C];   // left input of chain c in the previous row (its diag at column 0)
     int prevleft_s[C];
-    float right0;        // C == 2: chain 0's right edge -> chain 1's left at the next step
-    int right0_s;
-    float outv;          // right edge of the last chain (to lane+1 / next warp)
-    int outs;
+    float right[C];      // right edge of chain c at the previous step (chain c+1's left;
+    int right_s[C];      // right[C-1] goes to lane+1 / the next warp)
 };
+// Row samples of one step: C floats (x_r, x_{r-1}, ...).
+template <int C> struct XRow;
+template <> struct XRow<1> { float v[1]; };
+template <> struct XRow<2> { unsigned long long p[1]; };
+template <> struct XRow<4> { unsigned long long p[2]; };
+// slow path: samples of row r (any residue)
+template <int C>
+__device__ __forceinline__ XRow<C> load_xrow(const float* xs, int r, int Pd) {
+    XRow<C> x;
+    if constexpr (C == 1) x.v[0] = xs[r];
+    else {
+        const unsigned long long* xp = reinterpret_cast<const unsigned long long*>(xs);
+        x.p[0] = xp[xrow_index(r, Pd, 2)];
+        if constexpr (C == 4) x.p[1] = xp[xrow_index(r >= 2 ? r - 2 : r - 2 + Pd, Pd, 2)];
+    }
+    return x;
+}
+// fast path: step h of a rotation period starting at row r0, with xb[j] pointing
+// at row r0+j of residue class (r0+j) mod XC (rows inside one round, no wrap)
+template <int C, int h>
+__device__ __forceinline__ XRow<C> load_xrow_fast(const float* const (&xb)[xrow_floats(C)]) {
+    XRow<C> x;
+    if constexpr (C == 1) x.v[0] = xb[0][h];
+    else {
+        const unsigned long long* xp = reinterpret_cast<const unsigned long long*>(xb[h & 1]);
+        x.p[0] = xp[h >> 1];
+        if constexpr (C == 4) x.p[1] = xp[(h >> 1) - 1];
+    }
+    return x;
+}
 
 // One row of the lane's strips (Eq. 1) at rotation offset H: reads the
-// row at offset H, leaves the new row at offset H+1.
-// C == 1: per cell FADD, FMNMX3, FFMA (3 SASS).  C == 2: per cell pair FADD2,
-// 2x FMNMX3, FFMA2 (2 SASS/cell).  xx: row sample(s); lin: chain 0's left input.
+// row at offset H, leaves the new row at offset H+1.  lin: chain 0's left input.
+// C == 1: per cell FADD, FMNMX3, FFMA (3 SASS); C >= 2: per cell pair FADD2,
+// 2x FMNMX3, FFMA2 (2 SASS/cell); the NP pairs are independent within the step.
 template <int C, int WC, bool FMA, bool TRACE, int H>
-__device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, WC>& Y, unsigned long long xx,
+__device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, WC>& Y, const XRow<C>& x,
                                           float lin, int lins, LaneScalars<C>& ls) {
     using RR = RotRow<C, WC, TRACE>;
-    if constexpr (C == 1) {
-        const float xv = __uint_as_float((unsigned)xx);
-        float left = lin, diag = ls.prevleft[0];
-        int sl = lins, sd = ls.prevleft_s[0];
-        ls.prevleft[0] = lin;
-        ls.prevleft_s[0] = lins;
+    constexpr int NP = RR::NP;
+    float left[C], pd[C];
+    int sl[C], psd[C];
 #pragma unroll
-        for (int w = 0; w < WC; ++w) {
-            const int ku = RR::slot(w, H), kd = RR::slot(w - 1, H);   // up slot; diag slot (= output slot)
-            const float up = R.D[ku];
-            const float dg = (w == 0) ? diag : R.D[kd];
-            const float m = min3f(dg, up, left);
-            const float v = cell1<FMA>(xv, Y.Y[w], m);
+    for (int c = 0; c < C; ++c) {
+        left[c] = (c == 0) ? lin : ls.right[c - 1];
+        sl[c] = (c == 0) ? lins : ls.right_s[c - 1];
+        pd[c] = ls.prevleft[c];
+        psd[c] = ls.prevleft_s[c];
+        ls.prevleft[c] = left[c];
+        ls.prevleft_s[c] = sl[c];
+    }
+#pragma unroll
+    for (int w = 0; w < WC; ++w) {
+        const int ku = RR::slot(w, H), kd = RR::slot(w - 1, H);   // up slot; diag slot (= output slot)
+        if constexpr (C == 1) {
+            const float up = R.D[0][ku];
+            const float dg = (w == 0) ? pd[0] : R.D[0][kd];
+            const float m = min3f(dg, up, left[0]);
+            const float v = cell1<FMA>(x.v[0], Y.Y[0][w], m);
             if constexpr (TRACE) {
                 const int su = R.S[0][ku];
-                const int sdg = (w == 0) ? sd : R.S[0][kd];
-                const int sv = (dg == m) ? sdg : ((up == m) ? su : sl);
+                const int sdg = (w == 0) ? psd[0] : R.S[0][kd];
+                const int sv = (dg == m) ? sdg : ((up == m) ? su : sl[0]);
                 R.S[0][kd] = sv;
-                sl = sv;
+                sl[0] = sv;
             }
-            R.D[kd] = v;
-            left = v;
-        }
-        ls.outv = left;
-        ls.outs = sl;
-    } else {
-        float l0 = lin, l1 = ls.right0;
-        const float pd0 = ls.prevleft[0], pd1 = ls.prevleft[1];
-        const int psd0 = ls.prevleft_s[0], psd1 = ls.prevleft_s[1];
-        int sl0 = lins, sl1 = ls.right0_s;
-        ls.prevleft[0] = l0;
-        ls.prevleft[1] = l1;
-        ls.prevleft_s[0] = sl0;
-        ls.prevleft_s[1] = sl1;
+            R.D[0][kd] = v;
+            left[0] = v;
+        } else {
 #pragma unroll
-        for (int w = 0; w < WC; ++w) {
-            const int ku = RR::slot(w, H), kd = RR::slot(w - 1, H);
-            const float u0v = lo32(R.D[ku]), u1v = hi32(R.D[ku]);
-            const float d0 = (w == 0) ? pd0 : lo32(R.D[kd]);
-            const float d1 = (w == 0) ? pd1 : hi32(R.D[kd]);
-            const float m0 = min3f(d0, u0v, l0);
-            const float m1 = min3f(d1, u1v, l1);
-            unsigned long long tt, vv;
-            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(xx), "l"(Y.Y[w]));
-            if (FMA) {
-                asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(vv) : "l"(tt), "l"(pk(m0, m1)));
-            } else {
-                const float t0v = lo32(tt), t1v = hi32(tt);
-                vv = pk(__fadd_rn(__fmul_rn(t0v, t0v), m0), __fadd_rn(__fmul_rn(t1v, t1v), m1));
+            for (int p = 0; p < NP; ++p) {
+                const int c0 = 2 * p, c1 = 2 * p + 1;
+                const float u0 = lo32(R.D[p][ku]), u1 = hi32(R.D[p][ku]);
+                const float d0 = (w == 0) ? pd[c0] : lo32(R.D[p][kd]);
+                const float d1 = (w == 0) ? pd[c1] : hi32(R.D[p][kd]);
+                const float m0 = min3f(d0, u0, left[c0]);
+                const float m1 = min3f(d1, u1, left[c1]);
+                const unsigned long long vv = cell2<FMA>(x.p[p], Y.Y[p][w], m0, m1);
+                if constexpr (TRACE) {
+                    const int su0 = R.S[c0][ku], su1 = R.S[c1][ku];
+                    const int sd0 = (w == 0) ? psd[c0] : R.S[c0][kd];
+                    const int sd1 = (w == 0) ? psd[c1] : R.S[c1][kd];
+                    const int sv0 = (d0 == m0) ? sd0 : ((u0 == m0) ? su0 : sl[c0]);
+                    const int sv1 = (d1 == m1) ? sd1 : ((u1 == m1) ? su1 : sl[c1]);
+                    R.S[c0][kd] = sv0;
+                    R.S[c1][kd] = sv1;
+                    sl[c0] = sv0;
+                    sl[c1] = sv1;
+                }
+                R.D[p][kd] = vv;
+                left[c0] = lo32(vv);
+                left[c1] = hi32(vv);
             }
-            if constexpr (TRACE) {
-                const int su0 = R.S[0][ku], su1 = R.S[1][ku];
-                const int sd0 = (w == 0) ? psd0 : R.S[0][kd];
-                const int sd1 = (w == 0) ? psd1 : R.S[1][kd];
-                const int sv0 = (d0 == m0) ? sd0 : ((u0v == m0) ? su0 : sl0);
-                const int sv1 = (d1 == m1) ? sd1 : ((u1v == m1) ? su1 : sl1);
-                R.S[0][kd] = sv0;
-                R.S[1][kd] = sv1;
-                sl0 = sv0;
-                sl1 = sv1;
-            }
-            R.D[kd] = vv;
-            l0 = lo32(vv);
-            l1 = hi32(vv);
         }
-        ls.right0 = l0;
-        ls.right0_s = sl0;
-        ls.outv = l1;
-        ls.outs = sl1;
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        ls.right[c] = left[c];
+        ls.right_s[c] = sl[c];
     }
 }
 
-// Load the WC reference samples of strip `strip` (+inf beyond Malloc).
+// Reference samples of strip `strip` (+inf beyond Malloc).
 template <int WC>
-__device__ __forceinline__ void load_strip_any(const float* __restrict__ Yg, int Malloc, long strip, float (&y)[WC]) {
+__device__ __forceinline__ void load_strip(const float* __restrict__ Yg, int Malloc, long strip, float (&y)[WC]) {
     const long col0 = strip * WC;
 #pragma unroll
     for (int w = 0; w < WC; ++w) y[w] = (col0 + w < (long)Malloc) ? __ldg(Yg + col0 + w) : INFINITY;
 }
 
-// Round transition of chain c at rotation offset 0: new strip (reload y),
-// virtual row -1 = 0.
+// Round transition of chain c (rotation offset 0): new strip (reload y), virtual
+// row -1 = 0 (and S(-1, j) = j+1, so that row 0 gets S = j).
 template <int C, int WC, bool TRACE>
 __device__ __forceinline__ void enter_strip(RotRow<C, WC, TRACE>& row, Ys<C, WC>& Y, int c, long strip, bool live,
                                             const float* __restrict__ Yg, int Malloc, LaneScalars<C>& ls) {
     float y[WC];
-    if (live) load_strip_any<WC>(Yg, Malloc, strip, y);
+    if (live) load_strip<WC>(Yg, Malloc, strip, y);
     else {
 #pragma unroll
         for (int w = 0; w < WC; ++w) y[w] = INFINITY;
     }
 #pragma unroll
-    for (int w = 0; w < WC; ++w) {
-        Y.set(c, w, y[w]);
-        row.set_d(c, w, 0.0f);
-        row.set_s(c, w, (int)(strip * WC) + w + 1);   // S(-1, j) = j+1, so row 0 gets S = j
+    for (int w = 0; w < WC; ++w) Y.set(c, w, y[w]);
+    row.set_all(c, 0.0f);
+    if constexpr (TRACE) {
+#pragma unroll
+        for (int w = 0; w < WC + 1; ++w) row.S[c][w] = (int)(strip * WC) + w + 1;
     }
-    ls.prevleft[c] = 0.0f;                // D(-1, col0-1) = 0
+    ls.prevleft[c] = 0.0f;                 // D(-1, col0-1) = 0
     ls.prevleft_s[c] = (int)(strip * WC);
 }
 
 // Fold the last row of chain c (rotation offset 0) into (best, bestcol, beststart):
 // strict '<' keeps the smallest column on ties (strips are visited in increasing
-// column order).
+// column order).  The row minimum is found first so the argmin scan is rare.
 template <int C, int WC, bool TRACE>
 __device__ __forceinline__ void fold_last_row(const RotRow<C, WC, TRACE>& row, int c, int col0, float& best,
                                               int& bestcol, int& beststart) {
+    float m = row.d(c, 0);
 #pragma unroll
-    for (int w = 0; w < WC; ++w) {
-        const float v = row.d(c, w);
-        if (v < best) {
-            best = v;
-            bestcol = col0 + w;
-            beststart = row.s(c, w);
+    for (int w = 1; w < WC; ++w) m = fminf(m, row.d(c, w));
+    if (m < best) {
+        best = m;
+#pragma unroll
+        for (int w = WC - 1; w >= 0; --w) {
+            if (row.d(c, w) == m) {
+                bestcol = col0 + w;
+                if constexpr (TRACE) beststart = row.S[c][w];
+            }
         }
     }
 }
@@ -378,7 +396,8 @@ __device__ __forceinline__ void unrotate1(RotRow<C, WC, TRACE>& R) {
     RotRow<C, WC, TRACE> T;
 #pragma unroll
     for (int w = 0; w < RR::U; ++w) {
-        T.D[w] = R.D[RR::slot(w, 1)];
+#pragma unroll
+        for (int p = 0; p < RR::NP; ++p) T.D[p][w] = R.D[p][RR::slot(w, 1)];
         if constexpr (TRACE) {
 #pragma unroll
             for (int c = 0; c < C; ++c) T.S[c][w] = R.S[c][RR::slot(w, 1)];
@@ -394,30 +413,24 @@ __device__ __forceinline__ void static_for(F&& f) {
         static_for<I + 1, N_>(f);
     }
 }
-
-// index of the (x_r, x_{r-1}) pair of row r in the parity-split layout
-__host__ __device__ __forceinline__ int xpair_index(int r, int Pd) { return (r & 1) * ((Pd + 1) >> 1) + (r >> 1); }
-
-// floor-mod
 __device__ __forceinline__ int fmod_pos(int a, int m) { int r = a % m; return r < 0 ? r + m : r; }
 // does the band interval [blo, blo+len) contain a band whose row (band mod Pd) == row?
-__device__ __forceinline__ bool hits_row(int blo, int len, int row, int Pd) {
-    return fmod_pos(row - blo, Pd) < len;
-}
+__device__ __forceinline__ bool hits_row(int blo, int len, int row, int Pd) { return fmod_pos(row - blo, Pd) < len; }
 
+// ============================================================================ kernel
 template <int C, int WC, bool FMA, bool TRACE, bool CLUSTER>
 __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
-    static_assert(C == 1 || C == 2, "C");
-    static_assert(((WC + 1) & WC) == 0 && (32 * C) % (WC + 1) == 0,
-                  "rotation period U = WC+1 must be a power of two dividing 32*C");
+    static_assert(C == 1 || C == 2 || C == 4, "chains per lane");
+    static_assert(((WC + 1) & WC) == 0 && (32 * C) % (WC + 1) == 0 && (WC + 1) % C == 0,
+                  "rotation period U = WC+1 must be a power of two dividing 32*C and divisible by C");
     extern __shared__ __align__(16) unsigned char smem[];
     using E = Entry<TRACE>;
     using RowT = RotRow<C, WC, TRACE>;
     constexpr int U = RowT::U;
 
     cg::cluster_group cluster = cg::this_cluster();
-    const int CL = (int)cluster.num_blocks();
-    const int rank = (int)cluster.block_rank();
+    const int CL = CLUSTER ? (int)cluster.num_blocks() : 1;
+    const int rank = CLUSTER ? (int)cluster.block_rank() : 0;
     const int q = blockIdx.x / CL;
     const int GW = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5;
@@ -426,7 +439,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     const int gw = rank * GW + warp;
     const int V = 32 * C * G;
     const int Pd = P.Pd, N = P.N, K = P.K, RS = P.RS;
-    const SmemLayout L = smem_layout(C, TRACE, GW, CL, Pd, RS);
+    const SmemLayout L = smem_layout(C, TRACE, GW, Pd, RS);
 
     int* pp = reinterpret_cast<int*>(smem + L.off_ctr);        // producer progress seen by warp w
     int* cp = pp + 32;                                          // consumer progress of w's successor
@@ -436,18 +449,16 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     Partial* red = reinterpret_cast<Partial*>(smem + L.off_red);
     E* infs = reinterpret_cast<E*>(smem + L.off_inf);
 
-    // ---- prologue: query -> smem (pairs (x_r, x_{r-1 mod Pd}) when C == 2), rings, counters
+    // ---- prologue: query rows -> smem, boundary ring = +inf, counters
     const float* xq = P.X + (long)q * N;
+    constexpr int XC = xrow_floats(C);
     for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
-        const float a = (r < N) ? xq[r] : 0.0f;
-        if (C == 2) {
-            // pairs (x_r, x_{r-1}); even rows then odd rows so that a warp's lanes
-            // (rows r, r-2, r-4, ...) read consecutive 8-byte words (no bank conflict)
-            const int rp = (r == 0) ? Pd - 1 : r - 1;
-            const float b = (rp < N) ? xq[rp] : 0.0f;
-            reinterpret_cast<float2*>(xs)[xpair_index(r, Pd)] = make_float2(a, b);
-        } else {
-            xs[r] = a;
+        float* dst = xs + (long)xrow_index(r, Pd, XC) * XC;
+#pragma unroll
+        for (int j = 0; j < XC; ++j) {
+            int rr = r - j;
+            if (rr < 0) rr += Pd;
+            dst[j] = (rr < N) ? xq[rr] : 0.0f;
         }
         E e;
         e.d = INFINITY;
@@ -463,7 +474,8 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
         const int g = rank * GW + threadIdx.x;   // successor of local warp threadIdx.x starts at 32C(g+1)
         cp[threadIdx.x] = 32 * C * (g + 1);
     }
-    cluster.sync();
+    if constexpr (CLUSTER) cluster.sync();
+    else __syncthreads();
 
     // ---- neighbours in the ring
     const bool has_succ_ring = (gw < G - 1);      // successor is a ring warp (else: the wrap)
@@ -477,9 +489,12 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
             succ_ring = cluster.map_shared_rank(ring, rank + 1);
             succ_pp = cluster.map_shared_rank(pp, rank + 1);
         }
-    } else {
+    } else if constexpr (CLUSTER) {
         succ_ring = cluster.map_shared_rank(bnd, 0);         // boundary ring of rank 0
         succ_pp = cluster.map_shared_rank(pp, 0);            // pp[0] of rank 0
+    } else {
+        succ_ring = bnd;
+        succ_pp = pp;
     }
     int* pred_cp = nullptr;                                   // where we report consumption
     if (gw > 0) pred_cp = (warp > 0) ? cp + warp - 1 : cluster.map_shared_rank(cp + GW - 1, rank - 1);
@@ -490,32 +505,29 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     const int u_last = V - 1;
     const int Mtot_bands = P.Pr * Pd;
 
-    // ---- per-lane state (the strip's row in a rotating register file)
+    // ---- per-lane state
     RowT R;
     Ys<C, WC> Y;
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-        if constexpr (C == 1) R.D[k] = INFINITY;
-        else R.D[k] = pk(INFINITY, INFINITY);
-        if constexpr (TRACE) {
-#pragma unroll
-            for (int c = 0; c < C; ++c) R.S[c][k] = 0;
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < C; ++c)
+    for (int c = 0; c < C; ++c) {
+        R.set_all(c, INFINITY);
 #pragma unroll
         for (int w = 0; w < WC; ++w) Y.set(c, w, INFINITY);
-    LaneScalars<C> ls;
+        if constexpr (TRACE) {
 #pragma unroll
-    for (int c = 0; c < C; ++c) { ls.prevleft[c] = INFINITY; ls.prevleft_s[c] = 0; }
-    ls.right0 = INFINITY; ls.right0_s = 0; ls.outv = INFINITY; ls.outs = 0;
+            for (int k = 0; k < U; ++k) R.S[c][k] = 0;
+        }
+    }
+    LaneScalars<C> ls;
     float best[C];
     int bestcol[C], beststart[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) { best[c] = INFINITY; bestcol[c] = 0x7fffffff; beststart[c] = 0; }
+    for (int c = 0; c < C; ++c) {
+        ls.prevleft[c] = INFINITY; ls.prevleft_s[c] = 0; ls.right[c] = INFINITY; ls.right_s[c] = 0;
+        best[c] = INFINITY; bestcol[c] = 0x7fffffff; beststart[c] = 0;
+    }
 
-    // band of chain 0 at this warp's first step t = u_min
+    // band / row / round of chain 0 at this warp's first step t = u_min
     int b0 = -C * lane;
     int p0 = (b0 < 0) ? -1 : 0;
     int r0 = (b0 < 0) ? b0 + Pd : 0;
@@ -530,11 +542,11 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     const int last_end = 32 * C * (G - 1) + span;        // = t_end of warp G-1
     const unsigned FULL = 0xffffffffu;
 
-    // One step on the slow path: per-lane round transitions / last-row folds may occur.
+    // One step on the slow path: per-lane round transitions / last-row folds.
     auto slow_step = [&](int t) {
-        float lin = __shfl_up_sync(FULL, ls.outv, 1);
+        float lin = __shfl_up_sync(FULL, ls.right[C - 1], 1);
         int lins = 0;
-        if constexpr (TRACE) lins = __shfl_up_sync(FULL, ls.outs, 1);
+        if constexpr (TRACE) lins = __shfl_up_sync(FULL, ls.right_s[C - 1], 1);
         if (lane == 0) {
             E e;
             if (gw == 0) {
@@ -546,30 +558,32 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
             lin = e.d;
             if constexpr (TRACE) lins = e.s;
         }
-        const int r1 = (r0 == 0) ? Pd - 1 : r0 - 1;   // chain 1 row
-        const int p1 = (r0 == 0) ? p0 - 1 : p0;       // chain 1 round
-        if (r0 == 0) enter_strip<C, WC, TRACE>(R, Y, 0, (long)p0 * V + u0, p0 < P.Pr, P.Y, P.Malloc, ls);
-        if (C == 2 && r1 == 0)
-            enter_strip<C, WC, TRACE>(R, Y, C - 1, (long)p1 * V + u0 + 1, p1 < P.Pr, P.Y, P.Malloc, ls);
-        unsigned long long xx;
-        if constexpr (C == 2) xx = reinterpret_cast<const unsigned long long*>(xs)[xpair_index(r0, Pd)];
-        else xx = __float_as_uint(xs[r0]);
-        row_cells<C, WC, FMA, TRACE, 0>(R, Y, xx, lin, lins, ls);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {           // chain c is at row r0-c of round pc
+            const int rc = (r0 >= c) ? r0 - c : r0 - c + Pd;
+            const int pc = (r0 >= c) ? p0 : p0 - 1;
+            if (rc == 0) enter_strip<C, WC, TRACE>(R, Y, c, (long)pc * V + u0 + c, pc < P.Pr, P.Y, P.Malloc, ls);
+        }
+        const XRow<C> x = load_xrow<C>(xs, r0, Pd);
+        row_cells<C, WC, FMA, TRACE, 0>(R, Y, x, lin, lins, ls);
         unrotate1<C, WC, TRACE>(R);
-        if (r0 == N - 1 && p0 >= 0 && p0 < P.Pr)
-            fold_last_row<C, WC, TRACE>(R, 0, (int)(((long)p0 * V + u0) * WC), best[0], bestcol[0], beststart[0]);
-        if (C == 2 && r1 == N - 1 && p1 >= 0 && p1 < P.Pr)
-            fold_last_row<C, WC, TRACE>(R, C - 1, (int)(((long)p1 * V + u0 + 1) * WC), best[C - 1],
-                                        bestcol[C - 1], beststart[C - 1]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int rc = (r0 >= c) ? r0 - c : r0 - c + Pd;
+            const int pc = (r0 >= c) ? p0 : p0 - 1;
+            if (rc == N - 1 && pc >= 0 && pc < P.Pr)
+                fold_last_row<C, WC, TRACE>(R, c, (int)(((long)pc * V + u0 + c) * WC), best[c], bestcol[c],
+                                            beststart[c]);
+        }
         if (lane == 31) {
             E e;
-            e.d = ls.outv;
-            if constexpr (TRACE) e.s = ls.outs;
+            e.d = ls.right[C - 1];
+            if constexpr (TRACE) e.s = ls.right_s[C - 1];
             if (has_succ_ring) {
                 succ_ring[t & (RS - 1)] = e;
             } else {
                 const int bl = b0 - (C - 1);               // band of the last chain
-                if (bl >= 0 && bl < Mtot_bands) succ_ring[(C == 2) ? r1 : r0] = e;
+                if (bl >= 0 && bl < Mtot_bands) succ_ring[fmod_pos(bl, Pd)] = e;
             }
         }
         ++b0;
@@ -585,73 +599,68 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
         if (lane == 31 && has_succ_ring) spin_until_geq<CLUSTER>(cp + warp, t0 + K - RS + 1, 3);
         __syncwarp();
 
-        // ---- fast chunk: no lane of this warp crosses row 0 (round transition) or
-        // row N-1 (last-row fold) -> warp-uniform, branch-free steps
-        const int blo = t0 - u_max, blen = K + 32 * C - 1;
-        const bool fast = !hits_row(blo, blen, 0, Pd) && !hits_row(blo, blen, N - 1, Pd);
-        if (fast) {
-            // Warp-uniform ring addressing, one base pointer per rotation period:
-            // lane 0 reads its left input for step t from slot t-1 of its inbox (or
-            // row t-u_min of the boundary ring for warp 0; +inf entries in round 0),
-            // lane 31 writes its right edge of step t to slot t of the successor's
-            // inbox (or row t-u_max of the boundary ring).  t0 and the period start
-            // are multiples of U, and U divides RS, so only the first read of a
-            // period can wrap around the inbox.
-            const int in_row = fmod_pos(t0 - u_min, Pd);
-            const bool lane0_inf = (gw == 0) && (t0 < Pd);
-            const int out_row = fmod_pos(t0 - u_max, Pd);
-            const unsigned long long* xpe = reinterpret_cast<const unsigned long long*>(xs) + xpair_index(r0, Pd);
-            const unsigned long long* xpo = reinterpret_cast<const unsigned long long*>(xs) + xpair_index(r0 + 1, Pd);
-            const float* x1 = xs + r0;
+        // ---- per rotation period (U steps): "fast" when no lane of this warp crosses
+        // row 0 (round transition) or row N-1 (last-row fold) inside it ->
+        // warp-uniform, branch-free steps; otherwise U per-lane slow steps.
 #pragma unroll 1
-            for (int s = 0; s < K; s += U) {
-                const int tg = t0 + s;
+        for (int s = 0; s < K; s += U) {
+            const int tg = t0 + s;
+            const int blo = tg - u_max, blen = U + 32 * C - 1;
+            const bool fast = !hits_row(blo, blen, 0, Pd) && !hits_row(blo, blen, N - 1, Pd);
+            if (fast) {
+                // Warp-uniform ring addressing: lane 0 reads its left input for step t
+                // from slot t-1 of its inbox (or row t-u_min of the boundary ring for
+                // warp 0; +inf entries in round 0), lane 31 writes its right edge of
+                // step t to slot t of the successor's inbox (or row t-u_max of the
+                // boundary ring).  tg is a multiple of U and U divides RS, so only the
+                // first read of a period can wrap around the inbox.
                 const E* ib0;
                 const E* ib1;
                 if (gw == 0) {
-                    ib0 = lane0_inf ? infs : bnd + in_row + s;
+                    ib0 = (tg < Pd) ? infs : bnd + fmod_pos(tg - u_min, Pd);
                     ib1 = ib0 + 1;
                 } else {
                     ib0 = my_in + ((tg - 1) & (RS - 1));
                     ib1 = my_in + (tg & (RS - 1));
                 }
-                E* ob = has_succ_ring ? succ_ring + (tg & (RS - 1)) : succ_ring + out_row + s;
+                E* ob = has_succ_ring ? succ_ring + (tg & (RS - 1)) : succ_ring + fmod_pos(tg - u_max, Pd);
+                // row samples: step h reads row r0+h, whose residue class (r0+h) mod XC
+                // is fixed per h since U is even
+                const float* xb[XC];
+#pragma unroll
+                for (int j = 0; j < XC; ++j) xb[j] = xs + (long)xrow_index(r0 + j, Pd, XC) * XC;
                 static_for<0, U>([&](auto hc) {
                     constexpr int h = decltype(hc)::value;
-                    float lin = __shfl_up_sync(FULL, ls.outv, 1);
+                    float lin = __shfl_up_sync(FULL, ls.right[C - 1], 1);
                     int lins = 0;
-                    if constexpr (TRACE) lins = __shfl_up_sync(FULL, ls.outs, 1);
+                    if constexpr (TRACE) lins = __shfl_up_sync(FULL, ls.right_s[C - 1], 1);
                     const E e = (h == 0) ? ib0[0] : ib1[h - 1];
                     if (lane == 0) {
                         lin = e.d;
                         if constexpr (TRACE) lins = e.s;
                     }
-                    unsigned long long xx;
-                    if constexpr (C == 2) xx = (h & 1) ? xpo[h >> 1] : xpe[h >> 1];
-                    else xx = __float_as_uint(x1[h]);
-                    row_cells<C, WC, FMA, TRACE, h>(R, Y, xx, lin, lins, ls);
+                    const XRow<C> x = load_xrow_fast<C, h>(xb);
+                    row_cells<C, WC, FMA, TRACE, h>(R, Y, x, lin, lins, ls);
                     if (lane == 31) {
                         E o;
-                        o.d = ls.outv;
-                        if constexpr (TRACE) o.s = ls.outs;
+                        o.d = ls.right[C - 1];
+                        if constexpr (TRACE) o.s = ls.right_s[C - 1];
                         ob[h] = o;
                     }
                 });
-                if constexpr (C == 2) { xpe += U / 2; xpo += U / 2; }
-                else x1 += U;
-            }
-            b0 += K;
-            r0 += K;                                     // may land exactly on the next round
-            if (r0 >= Pd) { r0 -= Pd; ++p0; }
-        } else {
+                b0 += U;
+                r0 += U;                                     // may land exactly on the next round
+                if (r0 >= Pd) { r0 -= Pd; ++p0; }
+            } else {
 #pragma unroll 1
-            for (int s = 0; s < K; ++s) slow_step(t0 + s);
+                for (int h = 0; h < U; ++h) slow_step(tg + h);
+            }
         }
 
         // ---- publish progress
         __syncwarp();
-        if (lane == 31) st_release<CLUSTER>(succ_pp, t0 + K, true);
-        if (lane == 0 && gw > 0) st_release<CLUSTER>(pred_cp, t0 + K, true);
+        if (lane == 31) st_release<CLUSTER>(succ_pp, t0 + K);
+        if (lane == 0 && gw > 0) st_release<CLUSTER>(pred_cp, t0 + K);
     }
 
     // ---- reduction of (cost, col[, start]) over chains, lanes, warps, cluster CTAs
@@ -672,14 +681,18 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     if (threadIdx.x == 0) {
         for (int w = 1; w < GW; ++w)
             if (better(red[w].cost, red[w].col, bc, bj)) { bc = red[w].cost; bj = red[w].col; bs = red[w].start; }
-        Partial* dst = cluster.map_shared_rank(red + 32, 0);
-        dst[rank] = Partial{bc, bj, bs, 0};
+        if constexpr (CLUSTER) {
+            Partial* dst = cluster.map_shared_rank(red + 32, 0);
+            dst[rank] = Partial{bc, bj, bs, 0};
+        }
     }
-    cluster.sync();
+    if constexpr (CLUSTER) cluster.sync();
     if (rank == 0 && threadIdx.x == 0) {
-        for (int k = 1; k < CL; ++k) {
-            const Partial pr = red[32 + k];
-            if (better(pr.cost, pr.col, bc, bj)) { bc = pr.cost; bj = pr.col; bs = pr.start; }
+        if constexpr (CLUSTER) {
+            for (int k = 1; k < CL; ++k) {
+                const Partial pr = red[32 + k];
+                if (better(pr.cost, pr.col, bc, bj)) { bc = pr.cost; bj = pr.col; bs = pr.start; }
+            }
         }
         if (*P.err_flag == 0) {
             if (bj == 0x7fffffff) { bj = 0; bs = 0; }   // every cell overflowed (raw mode only)

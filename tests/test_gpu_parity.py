@@ -78,6 +78,9 @@ SCHEDULES = [
     dict(OPT_PACKED=1, OPT_SEGMENT_W=62, OPT_LANES=2),
     dict(OPT_PACKED=1, OPT_SEGMENT_W=30, OPT_LANES=1, OPT_CLUSTER=8, OPT_CHUNK=16),
     dict(OPT_PACKED=1, OPT_SEGMENT_W=6, OPT_LANES=8, OPT_CHUNK=64),
+    dict(OPT_PACKED=2, OPT_SEGMENT_W=28, OPT_LANES=4),
+    dict(OPT_PACKED=2, OPT_SEGMENT_W=60, OPT_LANES=1, OPT_CLUSTER=2),
+    dict(OPT_PACKED=2, OPT_SEGMENT_W=28, OPT_LANES=2, OPT_RING=256),
 ]
 
 
@@ -97,7 +100,7 @@ def test_config1_bit_exact_all_schedules(fma, sched):
     (1, 1, 1), (3, 1, 1000), (2, 5, 1), (4, 7, 3), (5, 33, 97), (3, 100, 50),     # N > M
     (7, 129, 4097), (2, 300, 20001), (9, 61, 12345), (1, 2000, 2000), (33, 17, 555),
 ])
-@pytest.mark.parametrize("packed", [0, 1])
+@pytest.mark.parametrize("packed", [0, 1, 2])
 def test_ragged_shapes_bit_exact(Z, N, M, packed):
     rng = np.random.default_rng(Z * 1000 + N * 10 + M)
     Q = rng.standard_normal((Z, N)).astype(np.float32)
@@ -111,7 +114,7 @@ def test_quantised_inputs_ties():
     rng = np.random.default_rng(77)
     Q = rng.integers(0, 3, (16, 40)).astype(np.float32)
     Y = rng.integers(0, 3, 3000).astype(np.float32)
-    for packed in (0, 1):
+    for packed in (0, 1, 2):
         got = _gpu(Q, Y, trace=True, OPT_PACKED=packed)
         ref = oracle.sdtw(Q, Y, start=True, last_rows=True)
         assert np.array_equal(got[0], ref["cost"])
