@@ -58,7 +58,10 @@ enum {
     SDTW_OPT_CHUNK = 8,     /* steps between inter-warp hand-off checks, rounded to whole
                                rotation periods (WC+1 steps); 0 = auto (32) */
     SDTW_OPT_PROFILE = 9,   /* 1: time the DP kernel with CUDA events (sdtw_profile) */
-    SDTW_OPT_RING = 10      /* inter-warp hand-off ring entries (rounded up to a power of two); 0 = auto */
+    SDTW_OPT_RING = 10,     /* inter-warp hand-off ring entries (rounded up to a power of two); 0 = auto */
+    SDTW_OPT_SCHED = 11,    /* 0 auto; 1 one CTA (or cluster) per query; 2 persistent CTAs pulling
+                               (query, round-segment) units -- balances any Z over the SMs */
+    SDTW_OPT_SEGMENTS = 12  /* round segments per query under persistent scheduling; 0 = auto */
 };
 
 /* Install the reference Y[M] on the current device (copied into a

@@ -30,6 +30,8 @@ struct Options {
     int chunk = 0;
     int profile = 0;
     int ring = 0;
+    int sched = 0;       // 0 auto, 1 one CTA (or cluster) per query, 2 persistent segments
+    int segments = 0;
     cudaStream_t stream = 0;
 };
 Options g_opt;
@@ -46,6 +48,7 @@ struct Ctx {
     float* ws_x = nullptr;   size_t ws_x_n = 0;     // normalised queries
     unsigned char* ws_out = nullptr; size_t ws_out_n = 0;
     double* ws_part = nullptr;                      // reference partial sums + stats
+    unsigned char* ws_sched = nullptr; size_t ws_sched_n = 0;   // persistent scheduling state
     int* flag_d = nullptr;
     int* flag_h = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -120,29 +123,23 @@ int ptr_kind(const void* p) {
 using sdtw::DpParams;
 using sdtw::DpKernel;
 
-DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl) {
-    switch (C) {
-        case 1: return sdtw::pick_dp_c1(WC, fma, trace, cl);
-        case 2: return sdtw::pick_dp_c2(WC, fma, trace, cl);
-        case 4: return sdtw::pick_dp_c4(WC, fma, trace, cl);
-        default: return nullptr;
-    }
-}
+DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl) { return sdtw::pick_dp(C, WC, fma, trace, cl); }
 
 struct LaunchCfg {
     int C, WC, GW, CL, K, RS, Pd, Pr, smem;
+    int persistent, S, workers;
 };
 
 sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cfg) {
     const Options& o = g_opt;
     // chains per lane: 1 scalar, 2 = one f32x2 pair, 4 = two independent pairs
     int C = (o.packed < 0) ? 2 : (o.packed == 0 ? 1 : (o.packed == 1 ? 2 : 4));
-    int W = o.segment_w > 0 ? o.segment_w : (C == 4 ? 28 : (C == 2 ? 30 : 31));
+    int W = o.segment_w > 0 ? o.segment_w : (C == 4 ? 28 : (C == 2 ? 30 : 15));
     if (W % C != 0) return fail(SDTW_E_ARG, "segment width must be a multiple of the chains per lane");
     int WC = W / C;
     if (!pick_kernel(C, WC, true, false, false))
         return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) +
-                                    (C == 4 ? " (4 chains: 28,60)" : C == 2 ? " (packed: 6,14,30,62)" : " (scalar: 7,15,31)"));
+                                    (C == 4 ? " (4 chains: 28)" : C == 2 ? " (2 chains: 14, 30)" : " (scalar: 7, 15)"));
     int GW = o.lanes > 0 ? o.lanes : 4;
     int CL = o.cluster > 0 ? o.cluster : 1;
     if (GW < 1 || GW > 8 || CL < 1 || CL > 16) return fail(SDTW_E_ARG, "lanes (1..8) / cluster (1..16) out of range");
@@ -160,12 +157,31 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // inter-warp ring depth: deep enough to absorb one warp's round-transition
     // (slow) chunks without stalling its neighbours
     int RS = 1;
-    const int RSmin = std::max(4 * K, o.ring > 0 ? (int)o.ring : 1024);
+    const int RSmin = std::max(4 * K, o.ring > 0 ? (int)o.ring : 512);
     while (RS < RSmin) RS <<= 1;
-    const sdtw::SmemLayout L = sdtw::smem_layout(C, trace, GW, (int)Pd, RS);
+    const sdtw::SmemLayout L = sdtw::smem_layout(C, WC, trace, GW, (int)Pd, RS);
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
-    *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes};
-    (void)Z;
+    *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0};
+    // Persistent scheduling (default when a cluster is not requested): k resident CTAs
+    // per SM, k = min(occupancy, Z / SMs), pull (query, round-segment) units, so every SM
+    // carries the same load whatever Z mod #SMs is.
+    const int sched = o.sched;
+    if (sched == 2 || (sched == 0 && CL == 1 && Z >= ctx.sms && Pr >= 8)) {
+        if (CL != 1) return fail(SDTW_E_ARG, "persistent scheduling needs cluster = 1");
+        int occ = 0;
+        DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false);
+        cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32 * GW, L.bytes) != cudaSuccess || occ < 1) {
+            cudaGetLastError();
+            return fail(SDTW_E_CUDA, "occupancy query failed");
+        }
+        const int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(occ, Z / ctx.sms));
+        int S = o.segments > 0 ? o.segments : (int)std::max<int64_t>(1, std::min<int64_t>(16, Pr / 4));
+        if (S > Pr) S = (int)Pr;
+        cfg->persistent = 1;
+        cfg->S = S;
+        cfg->workers = (int)std::min<int64_t>((int64_t)per_sm * ctx.sms, Z * S);
+    }
     return SDTW_OK;
 }
 
@@ -175,7 +191,7 @@ sdtw_status launch_dp(const LaunchCfg& c, bool fma, bool trace, const DpParams& 
     if (c.CL > 8) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t lc;
     memset(&lc, 0, sizeof(lc));
-    lc.gridDim = dim3((unsigned)(p.Z * c.CL));
+    lc.gridDim = dim3((unsigned)(c.persistent ? c.workers : p.Z * c.CL));
     lc.blockDim = dim3((unsigned)(32 * c.GW));
     lc.dynamicSmemBytes = (size_t)c.smem;
     lc.stream = st;
@@ -264,9 +280,33 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.out_end = de;
     p.out_start = trace ? ds : nullptr;
     p.err_flag = ctx->flag_d;
+    p.persistent = cfg.persistent;
+    p.S = cfg.S;
+    p.counter = nullptr;
+    p.seg_done = nullptr;
+    p.bnd_g = nullptr;
+    p.cand = nullptr;
+    if (cfg.persistent) {
+        const size_t ent = trace ? 8 : 4;
+        const size_t nb = 256 + sizeof(int) * (size_t)Z + ent * (size_t)Z * cfg.Pd + 16 * (size_t)Z * cfg.S;
+        s = grow(&ctx->ws_sched, &ctx->ws_sched_n, nb);
+        if (s != SDTW_OK) return s;
+        unsigned char* b = ctx->ws_sched;
+        p.counter = reinterpret_cast<int*>(b);
+        p.seg_done = reinterpret_cast<int*>(b + 256);
+        p.cand = b + 256 + ((sizeof(int) * (size_t)Z + 255) / 256) * 256;
+        p.bnd_g = static_cast<unsigned char*>(p.cand) + 16 * (size_t)Z * cfg.S;
+        CK(cudaMemsetAsync(b, 0, 256 + sizeof(int) * (size_t)Z, st));
+    }
     if (o.profile) CK(cudaEventRecord(ctx->ev0, st));
     s = launch_dp(cfg, o.fma != 0, trace, p, st);
     if (s != SDTW_OK) return s;
+    if (cfg.persistent) {
+        sdtw::finalize_kernel<<<(unsigned)((Z + 127) / 128), 128, 0, st>>>(
+            static_cast<const sdtw::Partial*>(p.cand), (int)Z, cfg.S, ctx->flag_d, dc, de, trace ? ds : nullptr);
+        CK(cudaGetLastError());
+        g_launches++;
+    }
     if (o.profile) CK(cudaEventRecord(ctx->ev1, st));
     CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -399,6 +439,8 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_CHUNK: if (v < 0 || v > 256) break; g_opt.chunk = (int)v; return SDTW_OK;
         case SDTW_OPT_PROFILE: if (v != 0 && v != 1) break; g_opt.profile = (int)v; return SDTW_OK;
         case SDTW_OPT_RING: if (v < 0 || v > 16384) break; g_opt.ring = (int)v; return SDTW_OK;
+        case SDTW_OPT_SCHED: if (v < 0 || v > 2) break; g_opt.sched = (int)v; return SDTW_OK;
+        case SDTW_OPT_SEGMENTS: if (v < 0 || v > 4096) break; g_opt.segments = (int)v; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
     return fail(SDTW_E_ARG, "bad value for option " + std::to_string(key));
@@ -418,6 +460,8 @@ sdtw_status sdtw_get_option(int key, int64_t* v) {
         case SDTW_OPT_CHUNK: *v = g_opt.chunk; return SDTW_OK;
         case SDTW_OPT_PROFILE: *v = g_opt.profile; return SDTW_OK;
         case SDTW_OPT_RING: *v = g_opt.ring; return SDTW_OK;
+        case SDTW_OPT_SCHED: *v = g_opt.sched; return SDTW_OK;
+        case SDTW_OPT_SEGMENTS: *v = g_opt.segments; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
 }
@@ -448,6 +492,7 @@ void sdtw_release(void) {
     cudaFree(c.ws_x);
     cudaFree(c.ws_out);
     cudaFree(c.ws_part);
+    cudaFree(c.ws_sched);
     cudaFree(c.flag_d);
     cudaFreeHost(c.flag_h);
     cudaEventDestroy(c.ev0);

@@ -55,6 +55,16 @@ struct DpParams {
     int64_t* out_end;
     int64_t* out_start;    // TRACE only
     const int* err_flag;   // nonzero -> write no results
+    // persistent scheduling (persistent != 0): CTAs pull units u = s*Z + q (query q,
+    // rounds [s*Pr/S, (s+1)*Pr/S)) from *counter; consecutive segments of a query hand
+    // the boundary column over through bnd_g and seg_done[q]; every unit writes its
+    // (cost, col, start) candidate to cand[q*S + s] for the finalize kernel.
+    int persistent;
+    int S;
+    int* counter;
+    int* seg_done;
+    void* bnd_g;
+    void* cand;
 };
 
 template <bool TRACE> struct Entry { float d; };
@@ -115,6 +125,24 @@ __device__ __forceinline__ void spin_until_geq(const int* p, int need, int tag) 
     if (ld_acquire<CLUSTER>(p) >= need) return;
     spin_slow<CLUSTER>(p, need, tag);
 }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Per-hop scope: only hand-offs that cross a CTA boundary of the cluster pay the
+// cluster-scoped (L1-invalidating) acquire; hops inside a CTA stay CTA-scoped.
+__device__ __forceinline__ void spin_until_geq_hop(const int* p, int need, int tag, bool remote) {
+    if (remote) spin_until_geq<true>(p, need, tag);
+    else spin_until_geq<false>(p, need, tag);
+}
+__device__ __forceinline__ void st_release_hop(int* p, int v, bool remote) {
+    if (remote) st_release_cluster(p, v);
+    else st_release_cta(p, v);
+}
 
 // ------------------------------------------------------------ arithmetic
 __device__ __forceinline__ float lo32(unsigned long long r) {
@@ -173,13 +201,13 @@ __host__ __device__ __forceinline__ int xrow_index(int r, int Pd, int XC) {
 __host__ __device__ __forceinline__ constexpr int xrow_floats(int C) { return C == 1 ? 1 : 2; }
 
 struct SmemLayout {
-    int off_ctr, off_red, off_inf, off_x, off_bnd, off_ring, bytes;
+    int off_ctr, off_red, off_inf, off_x, off_bnd, off_ring, off_stage, bytes;
 };
-__host__ __device__ inline SmemLayout smem_layout(int C, bool trace, int GW, int Pd, int RS) {
+__host__ __device__ inline SmemLayout smem_layout(int C, int WC, bool trace, int GW, int Pd, int RS) {
     SmemLayout L;
     const int ent = trace ? 8 : 4;
     int o = 0;
-    L.off_ctr = o;  o += 2 * 32 * 4;                    // pp[32], cp[32]
+    L.off_ctr = o;  o += 3 * 32 * 4;                    // pp[32], cp[32], unit broadcast
     L.off_red = o;  o += 16 * (32 + 16);                // per-warp + per-rank partials
     L.off_inf = o;  o += 32 * 8;                        // +inf inbox entries (round 0)
     o = (o + 15) & ~15;
@@ -188,6 +216,8 @@ __host__ __device__ inline SmemLayout smem_layout(int C, bool trace, int GW, int
     L.off_bnd = o;  o += Pd * ent;
     o = (o + 15) & ~15;
     L.off_ring = o; o += GW * RS * ent;
+    o = (o + 15) & ~15;
+    L.off_stage = o; o += GW * 32 * C * WC * 4;         // next-round reference strips, per warp
     L.bytes = (o + 15) & ~15;
     return L;
 }
@@ -338,39 +368,46 @@ __device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, W
     }
 }
 
-// Reference samples of strip `strip` (+inf beyond Malloc).
-template <int WC>
-__device__ __forceinline__ void load_strip(const float* __restrict__ Yg, int Malloc, long strip, float (&y)[WC]) {
-    const long col0 = strip * WC;
-#pragma unroll
-    for (int w = 0; w < WC; ++w) y[w] = (col0 + w < (long)Malloc) ? __ldg(Yg + col0 + w) : INFINITY;
+// Stage the reference strips of round p for one warp (32*C strips of WC samples,
+// contiguous in global memory) into shared memory with cp.async (no registers,
+// no stall): issued one round ahead, consumed by the lanes' round transitions.
+template <int C, int WC>
+__device__ __forceinline__ void stage_round(float* stage, const float* __restrict__ Yg, int Malloc, int Pr, long V,
+                                            int u_min, int p, int lane) {
+    const long col0 = ((long)p * V + u_min) * WC;
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(stage);
+#pragma unroll 1
+    for (int i = lane; i < 32 * C * WC; i += 32) {
+        const long col = col0 + i;
+        if (p < Pr && col < (long)Malloc) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sbase + 4u * i), "l"(Yg + col) : "memory");
+        } else {
+            stage[i] = INFINITY;
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// Round transition of chain c (rotation offset 0): new strip (reload y), virtual
-// row -1 = 0 (and S(-1, j) = j+1, so that row 0 gets S = j).
+// Round transition of chain c (slow path, rotation offset 0): new strip (y from
+// the staged copy), virtual row -1 = 0, and S(-1, j) = j+1 so that row 0 gets S = j.
 template <int C, int WC, bool TRACE>
 __device__ __forceinline__ void enter_strip(RotRow<C, WC, TRACE>& row, Ys<C, WC>& Y, int c, long strip, bool live,
-                                            const float* __restrict__ Yg, int Malloc, LaneScalars<C>& ls) {
-    float y[WC];
-    if (live) load_strip<WC>(Yg, Malloc, strip, y);
-    else {
+                                            const float* ystage, LaneScalars<C>& ls) {
 #pragma unroll
-        for (int w = 0; w < WC; ++w) y[w] = INFINITY;
-    }
-#pragma unroll
-    for (int w = 0; w < WC; ++w) Y.set(c, w, y[w]);
+    for (int w = 0; w < WC; ++w) Y.set(c, w, live ? ystage[w] : INFINITY);
     row.set_all(c, 0.0f);
     if constexpr (TRACE) {
 #pragma unroll
-        for (int w = 0; w < WC + 1; ++w) row.S[c][w] = (int)(strip * WC) + w + 1;
+        for (int k = 0; k < WC + 1; ++k) row.S[c][k] = (int)(strip * WC) + k + 1;
     }
     ls.prevleft[c] = 0.0f;                 // D(-1, col0-1) = 0
     ls.prevleft_s[c] = (int)(strip * WC);
 }
 
-// Fold the last row of chain c (rotation offset 0) into (best, bestcol, beststart):
-// strict '<' keeps the smallest column on ties (strips are visited in increasing
-// column order).  The row minimum is found first so the argmin scan is rare.
+// Last-row fold of chain c (slow path, rotation offset 0) into (best, bestcol,
+// beststart): strict '<' keeps the smallest column on ties (strips are visited in
+// increasing column order).  The row minimum is found first; the argmin scan only
+// runs on a new best.
 template <int C, int WC, bool TRACE>
 __device__ __forceinline__ void fold_last_row(const RotRow<C, WC, TRACE>& row, int c, int col0, float& best,
                                               int& bestcol, int& beststart) {
@@ -431,7 +468,6 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = CLUSTER ? (int)cluster.num_blocks() : 1;
     const int rank = CLUSTER ? (int)cluster.block_rank() : 0;
-    const int q = blockIdx.x / CL;
     const int GW = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -439,7 +475,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     const int gw = rank * GW + warp;
     const int V = 32 * C * G;
     const int Pd = P.Pd, N = P.N, K = P.K, RS = P.RS;
-    const SmemLayout L = smem_layout(C, TRACE, GW, Pd, RS);
+    const SmemLayout L = smem_layout(C, WC, TRACE, GW, Pd, RS);
 
     int* pp = reinterpret_cast<int*>(smem + L.off_ctr);        // producer progress seen by warp w
     int* cp = pp + 32;                                          // consumer progress of w's successor
@@ -448,34 +484,6 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     E* ring = reinterpret_cast<E*>(smem + L.off_ring);
     Partial* red = reinterpret_cast<Partial*>(smem + L.off_red);
     E* infs = reinterpret_cast<E*>(smem + L.off_inf);
-
-    // ---- prologue: query rows -> smem, boundary ring = +inf, counters
-    const float* xq = P.X + (long)q * N;
-    constexpr int XC = xrow_floats(C);
-    for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
-        float* dst = xs + (long)xrow_index(r, Pd, XC) * XC;
-#pragma unroll
-        for (int j = 0; j < XC; ++j) {
-            int rr = r - j;
-            if (rr < 0) rr += Pd;
-            dst[j] = (rr < N) ? xq[rr] : 0.0f;
-        }
-        E e;
-        e.d = INFINITY;
-        if constexpr (TRACE) e.s = 0;
-        bnd[r] = e;
-    }
-    if (threadIdx.x < 32) {
-        E e;
-        e.d = INFINITY;
-        if constexpr (TRACE) e.s = 0;
-        infs[threadIdx.x] = e;
-        pp[threadIdx.x] = 0;
-        const int g = rank * GW + threadIdx.x;   // successor of local warp threadIdx.x starts at 32C(g+1)
-        cp[threadIdx.x] = 32 * C * (g + 1);
-    }
-    if constexpr (CLUSTER) cluster.sync();
-    else __syncthreads();
 
     // ---- neighbours in the ring
     const bool has_succ_ring = (gw < G - 1);      // successor is a ring warp (else: the wrap)
@@ -499,11 +507,76 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     int* pred_cp = nullptr;                                   // where we report consumption
     if (gw > 0) pred_cp = (warp > 0) ? cp + warp - 1 : cluster.map_shared_rank(cp + GW - 1, rank - 1);
     const E* my_in = (gw == 0) ? bnd : ring + warp * RS;
+    // does my inbound (outbound) hand-off cross a CTA boundary of the cluster?
+    const bool pred_remote = CLUSTER && warp == 0;          // previous rank, or the wrap from the last rank
+    const bool succ_remote = CLUSTER && warp == GW - 1;     // next rank, or the wrap to rank 0
     const int u_min = 32 * C * gw;                 // virtual lane of lane 0, chain 0
     const int u_max = u_min + 32 * C - 1;          // virtual lane of lane 31, last chain
     const int u0 = C * (32 * gw + lane);
     const int u_last = V - 1;
-    const int Mtot_bands = P.Pr * Pd;
+
+    constexpr int XC = xrow_floats(C);
+    int* unit_sh = pp + 64;                                     // broadcast of the grabbed unit
+    for (int unit_iter = 0;; ++unit_iter) {
+    // ---- which unit: (query q, rounds [pa, pb))
+    int q, seg = 0, pa = 0, pb = P.Pr;
+    if (P.persistent) {
+        if (threadIdx.x == 0) *unit_sh = atomicAdd(P.counter, 1);
+        __syncthreads();
+        const int u = *unit_sh;
+        __syncthreads();
+        if (u >= P.Z * P.S) break;
+        q = u % P.Z;
+        seg = u / P.Z;
+        pa = (int)((long)seg * P.Pr / P.S);
+        pb = (int)((long)(seg + 1) * P.Pr / P.S);
+        if (seg > 0 && threadIdx.x == 0) {                 // previous segment's boundary column
+            long n = 0;
+            while (ld_acquire_gpu(P.seg_done + q) < seg) {
+                __nanosleep(256);
+                if (++n == (1LL << 26)) { printf("sdtw watchdog: unit %d waits segment\n", u); __trap(); }
+            }
+        }
+        __syncthreads();
+    } else {
+        if (unit_iter > 0) break;
+        q = blockIdx.x / CL;
+    }
+    const int Pl = pb - pa;                                 // rounds in this unit
+    const int Mtot_bands = Pl * Pd;
+
+    // ---- prologue: query rows -> smem, boundary ring (+inf, or the previous
+    // segment's last column), counters
+    const float* xq = P.X + (long)q * N;
+    const E* bg = reinterpret_cast<const E*>(P.bnd_g) + (long)q * Pd;
+    for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
+        float* dst = xs + (long)xrow_index(r, Pd, XC) * XC;
+#pragma unroll
+        for (int j = 0; j < XC; ++j) {
+            int rr = r - j;
+            if (rr < 0) rr += Pd;
+            dst[j] = (rr < N) ? xq[rr] : 0.0f;
+        }
+        E e;
+        if (pa > 0) {
+            e = bg[r];
+        } else {
+            e.d = INFINITY;
+            if constexpr (TRACE) e.s = 0;
+        }
+        bnd[r] = e;
+    }
+    if (threadIdx.x < 32) {
+        E e;
+        e.d = INFINITY;
+        if constexpr (TRACE) e.s = 0;
+        infs[threadIdx.x] = e;
+        pp[threadIdx.x] = 0;
+        const int g = rank * GW + threadIdx.x;   // successor of local warp threadIdx.x starts at 32C(g+1)
+        cp[threadIdx.x] = 32 * C * (g + 1);
+    }
+    if constexpr (CLUSTER) cluster.sync();
+    else __syncthreads();
 
     // ---- per-lane state
     RowT R;
@@ -542,7 +615,14 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     const int last_end = 32 * C * (G - 1) + span;        // = t_end of warp G-1
     const unsigned FULL = 0xffffffffu;
 
-    // One step on the slow path: per-lane round transitions / last-row folds.
+    // Reference strips for the lanes' round transitions are staged in shared memory
+    // one round ahead (pf_round = round currently staged).
+    float* ystage = reinterpret_cast<float*>(smem + L.off_stage) + warp * (32 * C * WC);
+    int pf_round = 0;                                        // local round staged
+    stage_round<C, WC>(ystage, P.Y, P.Malloc, P.Pr, V, u_min, pa, lane);
+
+    // One step on the slow path (rotation offset 0 before and after): per-lane round
+    // transitions before, and last-row folds after, the step's cells.
     auto slow_step = [&](int t) {
         float lin = __shfl_up_sync(FULL, ls.right[C - 1], 1);
         int lins = 0;
@@ -550,7 +630,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
         if (lane == 0) {
             E e;
             if (gw == 0) {
-                if (p0 >= 1) e = my_in[r0];
+                if (p0 >= 1 || pa > 0) e = my_in[r0];
                 else { e.d = INFINITY; if constexpr (TRACE) e.s = 0; }
             } else {
                 e = my_in[(t - 1) & (RS - 1)];
@@ -562,7 +642,9 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
         for (int c = 0; c < C; ++c) {           // chain c is at row r0-c of round pc
             const int rc = (r0 >= c) ? r0 - c : r0 - c + Pd;
             const int pc = (r0 >= c) ? p0 : p0 - 1;
-            if (rc == 0) enter_strip<C, WC, TRACE>(R, Y, c, (long)pc * V + u0 + c, pc < P.Pr, P.Y, P.Malloc, ls);
+            if (rc == 0)
+                enter_strip<C, WC, TRACE>(R, Y, c, (long)(pa + pc) * V + u0 + c, pc < Pl,
+                                          ystage + (lane * C + c) * WC, ls);
         }
         const XRow<C> x = load_xrow<C>(xs, r0, Pd);
         row_cells<C, WC, FMA, TRACE, 0>(R, Y, x, lin, lins, ls);
@@ -571,8 +653,8 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
         for (int c = 0; c < C; ++c) {
             const int rc = (r0 >= c) ? r0 - c : r0 - c + Pd;
             const int pc = (r0 >= c) ? p0 : p0 - 1;
-            if (rc == N - 1 && pc >= 0 && pc < P.Pr)
-                fold_last_row<C, WC, TRACE>(R, c, (int)(((long)pc * V + u0 + c) * WC), best[c], bestcol[c],
+            if (rc == N - 1 && pc >= 0 && pc < Pl)
+                fold_last_row<C, WC, TRACE>(R, c, (int)(((long)(pa + pc) * V + u0 + c) * WC), best[c], bestcol[c],
                                             beststart[c]);
         }
         if (lane == 31) {
@@ -593,10 +675,10 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     for (int t0 = t_begin; t0 < t_end; t0 += K) {
         // ---- chunk-level flow control (one lane each), then converge
         if (lane == 0) {
-            if (gw > 0) spin_until_geq<CLUSTER>(pp + warp, min(t0 + K - 1, pred_end), 1);
-            else if (t0 + K - 1 >= Pd) spin_until_geq<CLUSTER>(pp, min(t0 + K - Pd + u_last, last_end), 2);
+            if (gw > 0) spin_until_geq_hop(pp + warp, min(t0 + K - 1, pred_end), 1, pred_remote);
+            else if (t0 + K - 1 >= Pd) spin_until_geq_hop(pp, min(t0 + K - Pd + u_last, last_end), 2, pred_remote);
         }
-        if (lane == 31 && has_succ_ring) spin_until_geq<CLUSTER>(cp + warp, t0 + K - RS + 1, 3);
+        if (lane == 31 && has_succ_ring) spin_until_geq_hop(cp + warp, t0 + K - RS + 1, 3, succ_remote);
         __syncwarp();
 
         // ---- per rotation period (U steps): "fast" when no lane of this warp crosses
@@ -617,7 +699,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                 const E* ib0;
                 const E* ib1;
                 if (gw == 0) {
-                    ib0 = (tg < Pd) ? infs : bnd + fmod_pos(tg - u_min, Pd);
+                    ib0 = (tg < Pd && pa == 0) ? infs : bnd + fmod_pos(tg - u_min, Pd);
                     ib1 = ib0 + 1;
                 } else {
                     ib0 = my_in + ((tg - 1) & (RS - 1));
@@ -652,15 +734,25 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                 r0 += U;                                     // may land exactly on the next round
                 if (r0 >= Pd) { r0 -= Pd; ++p0; }
             } else {
+                if (hits_row(blo, blen, 0, Pd)) {           // a transition reads the staged strips
+                    asm volatile("cp.async.wait_all;" ::: "memory");
+                    __syncwarp();
+                }
 #pragma unroll 1
                 for (int h = 0; h < U; ++h) slow_step(tg + h);
+            }
+            // the last lane of this warp has entered round pf_round: stage round pf_round+1
+            if (tg + U > pf_round * Pd + u_max + 1 && pf_round + 1 < Pl) {
+                ++pf_round;
+                __syncwarp();
+                stage_round<C, WC>(ystage, P.Y, P.Malloc, P.Pr, V, u_min, pa + pf_round, lane);
             }
         }
 
         // ---- publish progress
         __syncwarp();
-        if (lane == 31) st_release<CLUSTER>(succ_pp, t0 + K);
-        if (lane == 0 && gw > 0) st_release<CLUSTER>(pred_cp, t0 + K);
+        if (lane == 31) st_release_hop(succ_pp, t0 + K, succ_remote);
+        if (lane == 0 && gw > 0) st_release_hop(pred_cp, t0 + K, pred_remote);
     }
 
     // ---- reduction of (cost, col[, start]) over chains, lanes, warps, cluster CTAs
@@ -694,13 +786,47 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                 if (better(pr.cost, pr.col, bc, bj)) { bc = pr.cost; bj = pr.col; bs = pr.start; }
             }
         }
-        if (*P.err_flag == 0) {
+        if (P.persistent) {
+            reinterpret_cast<Partial*>(P.cand)[(long)q * P.S + seg] = Partial{bc, bj, bs, 0};
+        } else if (*P.err_flag == 0) {
             if (bj == 0x7fffffff) { bj = 0; bs = 0; }   // every cell overflowed (raw mode only)
             P.out_cost[q] = bc;
             P.out_end[q] = bj;
             if (TRACE && P.out_start) P.out_start[q] = bs;
         }
     }
+    if (P.persistent) {
+        // hand this segment's last column to the next segment of the query
+        if (seg + 1 < P.S) {
+            E* bo = reinterpret_cast<E*>(P.bnd_g) + (long)q * Pd;
+            for (int r = threadIdx.x; r < Pd; r += blockDim.x) bo[r] = bnd[r];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_gpu(P.seg_done + q, seg + 1);
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    }   // unit loop
+}
+
+// Persistent scheduling epilogue: per query, the lexicographic (cost, col) minimum
+// over its segments' candidates (and that candidate's start column).
+static __global__ void finalize_kernel(const Partial* __restrict__ cand, int Z, int S, const int* err_flag, float* out_cost,
+                                int64_t* out_end, int64_t* out_start) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Z || *err_flag) return;
+    Partial b = cand[(long)q * S];
+    for (int s = 1; s < S; ++s) {
+        const Partial c = cand[(long)q * S + s];
+        if (better(c.cost, c.col, b.cost, b.col)) b = c;
+    }
+    if (b.col == 0x7fffffff) { b.col = 0; b.start = 0; }   // every cell overflowed (raw mode only)
+    out_cost[q] = b.cost;
+    out_end[q] = b.col;
+    if (out_start) out_start[q] = b.start;
 }
 
 }  // namespace sdtw

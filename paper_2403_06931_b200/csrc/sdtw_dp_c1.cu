@@ -1,23 +1,18 @@
-// sdtw_dp_c1.cu -- instantiations of the DP kernel with 1 chain(s) per lane
-// (separate translation unit so the kernel variants compile in parallel).
+// sdtw_dp_c1.cu -- instantiations of the DP kernel with 1 chain(s) per lane, cost/end
+// (one translation unit per variant family so they compile in parallel).
 #include "sdtw_dp_pick.h"
 
 namespace sdtw {
 template <int WC>
-static DpKernel pick_w(bool fma, bool trace, bool cl) {
-    if (fma) {
-        if (trace) return cl ? sdtw_dp_kernel<1, WC, true, true, true> : sdtw_dp_kernel<1, WC, true, true, false>;
-        return cl ? sdtw_dp_kernel<1, WC, true, false, true> : sdtw_dp_kernel<1, WC, true, false, false>;
-    }
-    if (trace) return cl ? sdtw_dp_kernel<1, WC, false, true, true> : sdtw_dp_kernel<1, WC, false, true, false>;
+static DpKernel pick_w(bool fma, bool cl) {
+    if (fma) return cl ? sdtw_dp_kernel<1, WC, true, false, true> : sdtw_dp_kernel<1, WC, true, false, false>;
     return cl ? sdtw_dp_kernel<1, WC, false, false, true> : sdtw_dp_kernel<1, WC, false, false, false>;
 }
 
-DpKernel pick_dp_c1(int WC, bool fma, bool trace, bool cl) {
+DpKernel pick_dp_c1(int WC, bool fma, bool cl) {
     switch (WC) {
-        case 7: return pick_w<7>(fma, trace, cl);
-        case 15: return pick_w<15>(fma, trace, cl);
-        case 31: return pick_w<31>(fma, trace, cl);
+        case 7: return pick_w<7>(fma, cl);
+        case 15: return pick_w<15>(fma, cl);
         default: return nullptr;
     }
 }

@@ -1,0 +1,19 @@
+// sdtw_dp_c2t.cu -- instantiations of the DP kernel with 2 chain(s) per lane, with start-index traceback
+// (one translation unit per variant family so they compile in parallel).
+#include "sdtw_dp_pick.h"
+
+namespace sdtw {
+template <int WC>
+static DpKernel pick_w(bool fma, bool cl) {
+    if (fma) return cl ? sdtw_dp_kernel<2, WC, true, true, true> : sdtw_dp_kernel<2, WC, true, true, false>;
+    return cl ? sdtw_dp_kernel<2, WC, false, true, true> : sdtw_dp_kernel<2, WC, false, true, false>;
+}
+
+DpKernel pick_dp_c2t(int WC, bool fma, bool cl) {
+    switch (WC) {
+        case 7: return pick_w<7>(fma, cl);
+        case 15: return pick_w<15>(fma, cl);
+        default: return nullptr;
+    }
+}
+}  // namespace sdtw

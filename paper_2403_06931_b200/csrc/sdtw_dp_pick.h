@@ -1,10 +1,21 @@
-// sdtw_dp_pick.h -- kernel selection across the per-C instantiation units.
+// sdtw_dp_pick.h -- kernel selection across the instantiation units.
 #pragma once
 #include "sdtw_dp.cuh"
 
 namespace sdtw {
 typedef void (*DpKernel)(DpParams);
-DpKernel pick_dp_c1(int WC, bool fma, bool trace, bool cl);
-DpKernel pick_dp_c2(int WC, bool fma, bool trace, bool cl);
-DpKernel pick_dp_c4(int WC, bool fma, bool trace, bool cl);
+DpKernel pick_dp_c1(int WC, bool fma, bool cl);
+DpKernel pick_dp_c1t(int WC, bool fma, bool cl);
+DpKernel pick_dp_c2(int WC, bool fma, bool cl);
+DpKernel pick_dp_c2t(int WC, bool fma, bool cl);
+DpKernel pick_dp_c4(int WC, bool fma, bool cl);
+DpKernel pick_dp_c4t(int WC, bool fma, bool cl);
+inline DpKernel pick_dp(int C, int WC, bool fma, bool trace, bool cl) {
+    switch (C) {
+        case 1: return trace ? pick_dp_c1t(WC, fma, cl) : pick_dp_c1(WC, fma, cl);
+        case 2: return trace ? pick_dp_c2t(WC, fma, cl) : pick_dp_c2(WC, fma, cl);
+        case 4: return trace ? pick_dp_c4t(WC, fma, cl) : pick_dp_c4(WC, fma, cl);
+        default: return nullptr;
+    }
+}
 }  // namespace sdtw

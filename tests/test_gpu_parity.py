@@ -69,18 +69,21 @@ SCHEDULES = [
     dict(),                                                  # auto
     dict(OPT_PACKED=0, OPT_SEGMENT_W=7, OPT_LANES=1),
     dict(OPT_PACKED=0, OPT_SEGMENT_W=15, OPT_LANES=2, OPT_CHUNK=16),
-    dict(OPT_PACKED=0, OPT_SEGMENT_W=31, OPT_LANES=4),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=6, OPT_LANES=1, OPT_CHUNK=8),
+    dict(OPT_PACKED=0, OPT_SEGMENT_W=15, OPT_LANES=4, OPT_CLUSTER=2),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=14, OPT_LANES=1, OPT_CHUNK=8),
     dict(OPT_PACKED=1, OPT_SEGMENT_W=14, OPT_LANES=3),
     dict(OPT_PACKED=1, OPT_SEGMENT_W=14, OPT_LANES=2, OPT_CLUSTER=2),
     dict(OPT_PACKED=1, OPT_SEGMENT_W=30, OPT_LANES=4, OPT_CLUSTER=2),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=62, OPT_LANES=1, OPT_CLUSTER=4),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=62, OPT_LANES=2),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=30, OPT_LANES=1, OPT_CLUSTER=4),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=30, OPT_LANES=2, OPT_RING=128),
     dict(OPT_PACKED=1, OPT_SEGMENT_W=30, OPT_LANES=1, OPT_CLUSTER=8, OPT_CHUNK=16),
-    dict(OPT_PACKED=1, OPT_SEGMENT_W=6, OPT_LANES=8, OPT_CHUNK=64),
+    dict(OPT_PACKED=1, OPT_SEGMENT_W=14, OPT_LANES=8, OPT_CHUNK=64),
     dict(OPT_PACKED=2, OPT_SEGMENT_W=28, OPT_LANES=4),
-    dict(OPT_PACKED=2, OPT_SEGMENT_W=60, OPT_LANES=1, OPT_CLUSTER=2),
+    dict(OPT_PACKED=2, OPT_SEGMENT_W=28, OPT_LANES=1, OPT_CLUSTER=2),
     dict(OPT_PACKED=2, OPT_SEGMENT_W=28, OPT_LANES=2, OPT_RING=256),
+    dict(OPT_SCHED=2, OPT_SEGMENTS=3),                       # persistent units (3 segments per query)
+    dict(OPT_SCHED=2, OPT_SEGMENTS=2, OPT_PACKED=0, OPT_SEGMENT_W=7, OPT_LANES=2),
+    dict(OPT_SCHED=1),
 ]
 
 
@@ -107,6 +110,9 @@ def test_ragged_shapes_bit_exact(Z, N, M, packed):
     Y = rng.standard_normal(M).astype(np.float32)
     got = _gpu(Q, Y, trace=True, OPT_PACKED=packed)
     _check_exact(Q, Y, got, trace=True)
+    if M >= 4000:   # several round segments per query under the persistent scheduler
+        got = _gpu(Q, Y, trace=True, OPT_PACKED=packed, OPT_SCHED=2, OPT_SEGMENTS=3, OPT_LANES=1)
+        _check_exact(Q, Y, got, trace=True)
 
 
 def test_quantised_inputs_ties():
@@ -131,9 +137,12 @@ def test_config5_shape_traceback(N):
 
 
 def test_config2_full_batch_sampled():
-    """BASELINE config 2 in full (512 x 2,000 vs 100,000, default launch); oracle on 24 sampled queries."""
+    """BASELINE config 2 in full (512 x 2,000 vs 100,000, default launch); oracle on 24 sampled queries;
+    the one-ring-per-query schedule must give identical bits."""
     Q, Y = _inputs(512, 2000, 100_000, 2)
     c, e, _ = _gpu(Q, Y)
+    c1, e1, _ = _gpu(Q, Y, OPT_SCHED=1)
+    assert np.array_equal(c, c1) and np.array_equal(e, e1)
     idx = np.linspace(0, 511, 24).astype(int)
     ref = oracle.sdtw(Q[idx], Y, start=False, last_rows=True)
     _check_exact(Q[idx], Y, (c[idx], e[idx], None), ref=ref)
