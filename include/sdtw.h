@@ -61,7 +61,9 @@ enum {
     SDTW_OPT_RING = 10,     /* inter-warp hand-off ring entries (rounded up to a power of two); 0 = auto */
     SDTW_OPT_SCHED = 11,    /* 0 auto; 1 one CTA (or cluster) per query; 2 persistent CTAs pulling
                                (query, round-segment) units -- balances any Z over the SMs */
-    SDTW_OPT_SEGMENTS = 12  /* round segments per query under persistent scheduling; 0 = auto */
+    SDTW_OPT_SEGMENTS = 12, /* round segments per query under persistent scheduling; 0 = auto */
+    SDTW_OPT_WORKERS = 13   /* resident CTAs per SM under persistent scheduling; 0 = auto
+                               (min(occupancy, n_queries / #SMs)) */
 };
 
 /* Install the reference Y[M] on the current device (copied into a

@@ -7,6 +7,7 @@
 #include "../../include/sdtw.h"
 #include "sdtw_dp.cuh"
 #include "sdtw_dp_pick.h"
+#include "sdtw_dpq.cuh"
 #include "sdtw_prep.cuh"
 
 #include <atomic>
@@ -32,6 +33,7 @@ struct Options {
     int ring = 0;
     int sched = 0;       // 0 auto, 1 one CTA (or cluster) per query, 2 persistent segments
     int segments = 0;
+    int workers = 0;     // resident CTAs per SM under persistent scheduling (0 = auto)
     cudaStream_t stream = 0;
 };
 Options g_opt;
@@ -123,26 +125,40 @@ int ptr_kind(const void* p) {
 using sdtw::DpParams;
 using sdtw::DpKernel;
 
-DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl) { return sdtw::pick_dp(C, WC, fma, trace, cl); }
+// dual: the dual-query kernel (two queries per lane, C chains of scalar-y strips)
+DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl, bool dual = false) {
+    if (dual) {
+        if (cl) return nullptr;
+        return C == 1 ? sdtw::pick_dpq_c1(WC, fma, trace) : (C == 2 ? sdtw::pick_dpq_c2(WC, fma, trace) : nullptr);
+    }
+    return sdtw::pick_dp(C, WC, fma, trace, cl);
+}
 
 struct LaunchCfg {
     int C, WC, GW, CL, K, RS, Pd, Pr, smem;
     int persistent, S, workers;
+    int dual;        // two queries per lane (chains per lane = C)
+    int64_t units;   // rings per batch: queries, or query pairs when dual
 };
 
+// Schedule choice.  OPT_PACKED: 0 scalar (C=1), 1 two packed chains (C=2), 2 four
+// chains (C=4), 3 dual-query x 2 chains, 4 dual-query x 1 chain; -1 auto.
 sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cfg) {
     const Options& o = g_opt;
-    // chains per lane: 1 scalar, 2 = one f32x2 pair, 4 = two independent pairs
-    int C = (o.packed < 0) ? 2 : (o.packed == 0 ? 1 : (o.packed == 1 ? 2 : 4));
+    const int packed = o.packed < 0 ? 1 : o.packed;
+    const bool dual = packed >= 3;
+    int C = dual ? (packed == 3 ? 2 : 1) : (packed == 0 ? 1 : (packed == 1 ? 2 : 4));
     int W = o.segment_w > 0 ? o.segment_w : (C == 4 ? 28 : (C == 2 ? 30 : 15));
     if (W % C != 0) return fail(SDTW_E_ARG, "segment width must be a multiple of the chains per lane");
     int WC = W / C;
-    if (!pick_kernel(C, WC, true, false, false))
-        return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) +
-                                    (C == 4 ? " (4 chains: 28)" : C == 2 ? " (2 chains: 14, 30)" : " (scalar: 7, 15)"));
+    if (!pick_kernel(C, WC, true, false, false, dual))
+        return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) + " for this chain layout" +
+                                    (C == 4 ? " (28)" : C == 2 ? " (14, 30)" : " (7, 15)"));
+    const int64_t units = dual ? (Z + 1) / 2 : Z;
     int GW = o.lanes > 0 ? o.lanes : 4;
     int CL = o.cluster > 0 ? o.cluster : 1;
-    if (GW < 1 || GW > 8 || CL < 1 || CL > 16) return fail(SDTW_E_ARG, "lanes (1..8) / cluster (1..16) out of range");
+    if (GW < 1 || GW > (dual ? 12 : 8) || CL < 1 || CL > 16 || (dual && CL != 1))
+        return fail(SDTW_E_ARG, "lanes / cluster out of range for this kernel");
     // chunk = whole rotation periods (U = WC+1 steps), about the requested size
     const int U = WC + 1;
     const int Kreq = o.chunk > 0 ? o.chunk : 32;
@@ -159,39 +175,41 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     int RS = 1;
     const int RSmin = std::max(4 * K, o.ring > 0 ? (int)o.ring : 512);
     while (RS < RSmin) RS <<= 1;
-    const sdtw::SmemLayout L = sdtw::smem_layout(C, WC, trace, GW, (int)Pd, RS);
+    const sdtw::SmemLayout L = dual ? sdtw::smem_layout_q(C, WC, trace, GW, (int)Pd, RS)
+                                    : sdtw::smem_layout(C, WC, trace, GW, (int)Pd, RS);
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
-    *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0};
+    *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0, dual ? 1 : 0, units};
     // Persistent scheduling (default when a cluster is not requested): k resident CTAs
-    // per SM, k = min(occupancy, Z / SMs), pull (query, round-segment) units, so every SM
-    // carries the same load whatever Z mod #SMs is.
+    // per SM, k = min(occupancy, rings / SMs), pull (ring, round-segment) units, so every
+    // SM carries the same load whatever the batch size mod #SMs is.
     const int sched = o.sched;
-    if (sched == 2 || (sched == 0 && CL == 1 && Z >= ctx.sms && Pr >= 8)) {
+    if (sched == 2 || (sched == 0 && CL == 1 && units >= ctx.sms && Pr >= 8)) {
         if (CL != 1) return fail(SDTW_E_ARG, "persistent scheduling needs cluster = 1");
         int occ = 0;
-        DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false);
+        DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false, dual);
         cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32 * GW, L.bytes) != cudaSuccess || occ < 1) {
             cudaGetLastError();
             return fail(SDTW_E_CUDA, "occupancy query failed");
         }
-        const int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(occ, Z / ctx.sms));
+        const int per_sm = o.workers > 0 ? std::min(o.workers, occ)
+                                         : (int)std::max<int64_t>(1, std::min<int64_t>(occ, units / ctx.sms));
         int S = o.segments > 0 ? o.segments : (int)std::max<int64_t>(1, std::min<int64_t>(16, Pr / 4));
         if (S > Pr) S = (int)Pr;
         cfg->persistent = 1;
         cfg->S = S;
-        cfg->workers = (int)std::min<int64_t>((int64_t)per_sm * ctx.sms, Z * S);
+        cfg->workers = (int)std::min<int64_t>((int64_t)per_sm * ctx.sms, units * S);
     }
     return SDTW_OK;
 }
 
 sdtw_status launch_dp(const LaunchCfg& c, bool fma, bool trace, const DpParams& p, cudaStream_t st) {
-    DpKernel k = pick_kernel(c.C, c.WC, fma, trace, c.CL > 1);
+    DpKernel k = pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0);
     CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem));
     if (c.CL > 8) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t lc;
     memset(&lc, 0, sizeof(lc));
-    lc.gridDim = dim3((unsigned)(c.persistent ? c.workers : p.Z * c.CL));
+    lc.gridDim = dim3((unsigned)(c.persistent ? c.workers : c.units * c.CL));
     lc.blockDim = dim3((unsigned)(32 * c.GW));
     lc.dynamicSmemBytes = (size_t)c.smem;
     lc.stream = st;
@@ -242,10 +260,12 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     }
     CK(cudaMemsetAsync(ctx->flag_d, 0, sizeof(int), st));
     const float* xd = qd;
-    if (o.normalize) {
-        s = grow(&ctx->ws_x, &ctx->ws_x_n, nel);
+    const bool pad = cfg.dual && (Z & 1);       // odd batch: a zero dummy query completes the last pair
+    if (o.normalize || pad) {
+        s = grow(&ctx->ws_x, &ctx->ws_x_n, nel + (pad ? (size_t)N : 0));
         if (s != SDTW_OK) return s;
-        sdtw::znorm_rows_kernel<<<(unsigned)Z, 256, 0, st>>>(qd, ctx->ws_x, N, 1, ctx->flag_d);
+        if (pad) CK(cudaMemsetAsync(ctx->ws_x + nel, 0, (size_t)N * sizeof(float), st));
+        sdtw::znorm_rows_kernel<<<(unsigned)Z, 256, 0, st>>>(qd, ctx->ws_x, N, o.normalize, ctx->flag_d);
         xd = ctx->ws_x;
     } else {
         sdtw::znorm_rows_kernel<<<(unsigned)Z, 256, 0, st>>>(qd, const_cast<float*>(qd), N, 0, ctx->flag_d);
@@ -269,7 +289,8 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.X = xd;
     p.Y = ctx->ref;
     p.Malloc = (int)ctx->Malloc;
-    p.Z = (int)Z;
+    p.Z = (int)cfg.units;
+    p.Zq = (int)Z;
     p.N = (int)N;
     p.M = (int)ctx->M;
     p.Pd = cfg.Pd;
@@ -287,16 +308,18 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.bnd_g = nullptr;
     p.cand = nullptr;
     if (cfg.persistent) {
-        const size_t ent = trace ? 8 : 4;
-        const size_t nb = 256 + sizeof(int) * (size_t)Z + ent * (size_t)Z * cfg.Pd + 16 * (size_t)Z * cfg.S;
+        const size_t ent = (trace ? 8 : 4) * (cfg.dual ? 2 : 1);
+        const size_t R = (size_t)cfg.units;
+        const size_t done_b = ((sizeof(int) * R + 255) / 256) * 256;
+        const size_t nb = 256 + done_b + 16 * (size_t)Z * cfg.S + ent * R * cfg.Pd;
         s = grow(&ctx->ws_sched, &ctx->ws_sched_n, nb);
         if (s != SDTW_OK) return s;
         unsigned char* b = ctx->ws_sched;
         p.counter = reinterpret_cast<int*>(b);
         p.seg_done = reinterpret_cast<int*>(b + 256);
-        p.cand = b + 256 + ((sizeof(int) * (size_t)Z + 255) / 256) * 256;
+        p.cand = b + 256 + done_b;
         p.bnd_g = static_cast<unsigned char*>(p.cand) + 16 * (size_t)Z * cfg.S;
-        CK(cudaMemsetAsync(b, 0, 256 + sizeof(int) * (size_t)Z, st));
+        CK(cudaMemsetAsync(b, 0, 256 + done_b, st));
     }
     if (o.profile) CK(cudaEventRecord(ctx->ev0, st));
     s = launch_dp(cfg, o.fma != 0, trace, p, st);
@@ -432,15 +455,16 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_NORMALIZE: if (v != 0 && v != 1) break; g_opt.normalize = (int)v; return SDTW_OK;
         case SDTW_OPT_FMA: if (v != 0 && v != 1) break; g_opt.fma = (int)v; return SDTW_OK;
         case SDTW_OPT_SEGMENT_W: if (v < 0 || v > 64) break; g_opt.segment_w = (int)v; return SDTW_OK;
-        case SDTW_OPT_LANES: if (v < 0 || v > 16) break; g_opt.lanes = (int)v; return SDTW_OK;
+        case SDTW_OPT_LANES: if (v < 0 || v > 12) break; g_opt.lanes = (int)v; return SDTW_OK;
         case SDTW_OPT_CLUSTER: if (v < 0 || v > 16) break; g_opt.cluster = (int)v; return SDTW_OK;
         case SDTW_OPT_STREAM: g_opt.stream = reinterpret_cast<cudaStream_t>(v); return SDTW_OK;
-        case SDTW_OPT_PACKED: if (v < -1 || v > 2) break; g_opt.packed = (int)v; return SDTW_OK;
+        case SDTW_OPT_PACKED: if (v < -1 || v > 4) break; g_opt.packed = (int)v; return SDTW_OK;
         case SDTW_OPT_CHUNK: if (v < 0 || v > 256) break; g_opt.chunk = (int)v; return SDTW_OK;
         case SDTW_OPT_PROFILE: if (v != 0 && v != 1) break; g_opt.profile = (int)v; return SDTW_OK;
         case SDTW_OPT_RING: if (v < 0 || v > 16384) break; g_opt.ring = (int)v; return SDTW_OK;
         case SDTW_OPT_SCHED: if (v < 0 || v > 2) break; g_opt.sched = (int)v; return SDTW_OK;
         case SDTW_OPT_SEGMENTS: if (v < 0 || v > 4096) break; g_opt.segments = (int)v; return SDTW_OK;
+        case SDTW_OPT_WORKERS: if (v < 0 || v > 32) break; g_opt.workers = (int)v; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
     return fail(SDTW_E_ARG, "bad value for option " + std::to_string(key));
@@ -462,6 +486,7 @@ sdtw_status sdtw_get_option(int key, int64_t* v) {
         case SDTW_OPT_RING: *v = g_opt.ring; return SDTW_OK;
         case SDTW_OPT_SCHED: *v = g_opt.sched; return SDTW_OK;
         case SDTW_OPT_SEGMENTS: *v = g_opt.segments; return SDTW_OK;
+        case SDTW_OPT_WORKERS: *v = g_opt.workers; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
 }

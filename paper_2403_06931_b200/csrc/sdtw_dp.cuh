@@ -61,6 +61,7 @@ struct DpParams {
     // (cost, col, start) candidate to cand[q*S + s] for the finalize kernel.
     int persistent;
     int S;
+    int Zq;                // real number of queries (dual-query kernel: P.Z counts pairs)
     int* counter;
     int* seg_done;
     void* bnd_g;
@@ -199,6 +200,9 @@ __host__ __device__ __forceinline__ int xrow_index(int r, int Pd, int XC) {
     return (r % XC) * xrow_stride(Pd, XC) + r / XC;
 }
 __host__ __device__ __forceinline__ constexpr int xrow_floats(int C) { return C == 1 ? 1 : 2; }
+// residue classes of the layout: the lanes of a warp read rows r, r-C, r-2C, ... ->
+// one class per residue mod C keeps their words consecutive (conflict-free)
+__host__ __device__ __forceinline__ constexpr int xrow_classes(int C) { return C; }
 
 struct SmemLayout {
     int off_ctr, off_red, off_inf, off_x, off_bnd, off_ring, off_stage, bytes;
@@ -211,7 +215,7 @@ __host__ __device__ inline SmemLayout smem_layout(int C, int WC, bool trace, int
     L.off_red = o;  o += 16 * (32 + 16);                // per-warp + per-rank partials
     L.off_inf = o;  o += 32 * 8;                        // +inf inbox entries (round 0)
     o = (o + 15) & ~15;
-    L.off_x = o;    o += xrow_stride(Pd, xrow_floats(C)) * xrow_floats(C) * xrow_floats(C) * 4;
+    L.off_x = o;    o += xrow_stride(Pd, xrow_classes(C)) * xrow_classes(C) * xrow_floats(C) * 4;
     o = (o + 15) & ~15;
     L.off_bnd = o;  o += Pd * ent;
     o = (o + 15) & ~15;
@@ -278,21 +282,24 @@ __device__ __forceinline__ XRow<C> load_xrow(const float* xs, int r, int Pd) {
     if constexpr (C == 1) x.v[0] = xs[r];
     else {
         const unsigned long long* xp = reinterpret_cast<const unsigned long long*>(xs);
-        x.p[0] = xp[xrow_index(r, Pd, 2)];
-        if constexpr (C == 4) x.p[1] = xp[xrow_index(r >= 2 ? r - 2 : r - 2 + Pd, Pd, 2)];
+        x.p[0] = xp[xrow_index(r, Pd, C)];
+        if constexpr (C == 4) x.p[1] = xp[xrow_index(r >= 2 ? r - 2 : r - 2 + Pd, Pd, C)];
     }
     return x;
 }
 // fast path: step h of a rotation period starting at row r0, with xb[j] pointing
-// at row r0+j of residue class (r0+j) mod XC (rows inside one round, no wrap)
+// at row r0+j (residue class (r0+j) mod C, j < C); rows stay inside one round
 template <int C, int h>
-__device__ __forceinline__ XRow<C> load_xrow_fast(const float* const (&xb)[xrow_floats(C)]) {
+__device__ __forceinline__ XRow<C> load_xrow_fast(const float* const (&xb)[xrow_classes(C)]) {
     XRow<C> x;
     if constexpr (C == 1) x.v[0] = xb[0][h];
     else {
-        const unsigned long long* xp = reinterpret_cast<const unsigned long long*>(xb[h & 1]);
-        x.p[0] = xp[h >> 1];
-        if constexpr (C == 4) x.p[1] = xp[(h >> 1) - 1];
+        constexpr int j0 = h % C, o0 = h / C;                       // row r0+h
+        x.p[0] = reinterpret_cast<const unsigned long long*>(xb[j0])[o0];
+        if constexpr (C == 4) {
+            constexpr int k = h - 2, j1 = ((k % C) + C) % C, o1 = (k - j1) / C;   // row r0+h-2
+            x.p[1] = reinterpret_cast<const unsigned long long*>(xb[j1])[o1];
+        }
     }
     return x;
 }
@@ -516,6 +523,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     const int u_last = V - 1;
 
     constexpr int XC = xrow_floats(C);
+    constexpr int NC = xrow_classes(C);
     int* unit_sh = pp + 64;                                     // broadcast of the grabbed unit
     for (int unit_iter = 0;; ++unit_iter) {
     // ---- which unit: (query q, rounds [pa, pb))
@@ -550,7 +558,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     const float* xq = P.X + (long)q * N;
     const E* bg = reinterpret_cast<const E*>(P.bnd_g) + (long)q * Pd;
     for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
-        float* dst = xs + (long)xrow_index(r, Pd, XC) * XC;
+        float* dst = xs + (long)xrow_index(r, Pd, NC) * XC;
 #pragma unroll
         for (int j = 0; j < XC; ++j) {
             int rr = r - j;
@@ -670,6 +678,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
         }
         ++b0;
         if (++r0 == Pd) { r0 = 0; ++p0; }
+        __syncwarp();                                   // reconverge before the next step's SHFL
     };
 
     for (int t0 = t_begin; t0 < t_end; t0 += K) {
@@ -708,9 +717,9 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                 E* ob = has_succ_ring ? succ_ring + (tg & (RS - 1)) : succ_ring + fmod_pos(tg - u_max, Pd);
                 // row samples: step h reads row r0+h, whose residue class (r0+h) mod XC
                 // is fixed per h since U is even
-                const float* xb[XC];
+                const float* xb[NC];
 #pragma unroll
-                for (int j = 0; j < XC; ++j) xb[j] = xs + (long)xrow_index(r0 + j, Pd, XC) * XC;
+                for (int j = 0; j < NC; ++j) xb[j] = xs + (long)xrow_index(r0 + j, Pd, NC) * XC;
                 static_for<0, U>([&](auto hc) {
                     constexpr int h = decltype(hc)::value;
                     float lin = __shfl_up_sync(FULL, ls.right[C - 1], 1);

@@ -84,6 +84,10 @@ SCHEDULES = [
     dict(OPT_SCHED=2, OPT_SEGMENTS=3),                       # persistent units (3 segments per query)
     dict(OPT_SCHED=2, OPT_SEGMENTS=2, OPT_PACKED=0, OPT_SEGMENT_W=7, OPT_LANES=2),
     dict(OPT_SCHED=1),
+    dict(OPT_PACKED=3, OPT_SEGMENT_W=30, OPT_LANES=4),        # dual-query, 2 chains
+    dict(OPT_PACKED=3, OPT_SEGMENT_W=14, OPT_LANES=12, OPT_SCHED=2, OPT_SEGMENTS=2),
+    dict(OPT_PACKED=4, OPT_SEGMENT_W=15, OPT_LANES=2),        # dual-query, 1 chain
+    dict(OPT_PACKED=4, OPT_SEGMENT_W=7, OPT_LANES=1, OPT_SCHED=2, OPT_SEGMENTS=3),
 ]
 
 
@@ -103,7 +107,7 @@ def test_config1_bit_exact_all_schedules(fma, sched):
     (1, 1, 1), (3, 1, 1000), (2, 5, 1), (4, 7, 3), (5, 33, 97), (3, 100, 50),     # N > M
     (7, 129, 4097), (2, 300, 20001), (9, 61, 12345), (1, 2000, 2000), (33, 17, 555),
 ])
-@pytest.mark.parametrize("packed", [0, 1, 2])
+@pytest.mark.parametrize("packed", [0, 1, 2, 3, 4])
 def test_ragged_shapes_bit_exact(Z, N, M, packed):
     rng = np.random.default_rng(Z * 1000 + N * 10 + M)
     Q = rng.standard_normal((Z, N)).astype(np.float32)
@@ -120,7 +124,7 @@ def test_quantised_inputs_ties():
     rng = np.random.default_rng(77)
     Q = rng.integers(0, 3, (16, 40)).astype(np.float32)
     Y = rng.integers(0, 3, 3000).astype(np.float32)
-    for packed in (0, 1, 2):
+    for packed in (0, 1, 2, 3, 4):
         got = _gpu(Q, Y, trace=True, OPT_PACKED=packed)
         ref = oracle.sdtw(Q, Y, start=True, last_rows=True)
         assert np.array_equal(got[0], ref["cost"])
