@@ -25,7 +25,7 @@ LIB_PATH = os.path.join(_HERE, "libsdtw.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         "paper_2403_06931_b200: CUDA library %s is missing -- run "
-        "`python -m paper_2403_06931_b200.build` (or __graft_entry__.build()); "
+        "`python __graft_entry__.py` (or `python paper_2403_06931_b200/build.py`); "
         "there is no CPU fallback" % LIB_PATH)
 
 _lib = ctypes.CDLL(LIB_PATH)

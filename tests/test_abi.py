@@ -16,10 +16,19 @@ def _declared_symbols():
     return sorted(set(re.findall(r"\b(sdtw_[a-z_]+)\s*\(", hdr)))
 
 
+def _builder():
+    # by path: the package refuses to import before libsdtw.so exists (no CPU fallback)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_sdtw_build", os.path.join(ROOT, "paper_2403_06931_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 @pytest.fixture(scope="module")
 def lib():
-    from paper_2403_06931_b200 import build
-    path = build.build()
+    path = _builder().build()
     return ctypes.CDLL(path)
 
 
@@ -38,7 +47,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_library_is_sm100a_native(lib):
-    from paper_2403_06931_b200 import build
+    build = _builder()
     out = subprocess.run(["cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", build.LIB], capture_output=True, text=True).stdout
