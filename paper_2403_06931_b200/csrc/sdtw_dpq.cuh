@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(384) sdtw_dpq_kernel(const DpParams P) {
             seg = u / P.Z;
             pa = (int)((long)seg * P.Pr / P.S);
             pb = (int)((long)(seg + 1) * P.Pr / P.S);
-            if (seg > 0 && threadIdx.x == 0) {
+            if (seg > 0) {                                  // every thread polls: no split warps
                 long n = 0;
                 while (ld_acquire_gpu(P.seg_done + qp) < seg) {
                     __nanosleep(256);
@@ -378,12 +378,12 @@ __global__ void __launch_bounds__(384) sdtw_dpq_kernel(const DpParams P) {
         };
 
         for (int t0 = t_begin; t0 < t_end; t0 += K) {
-            if (lane == 0) {
-                if (gw > 0) spin_until_geq<false>(pp + warp, min(t0 + K - 1, pred_end), 1);
-                else if (t0 + K - 1 >= Pd) spin_until_geq<false>(pp, min(t0 + K - Pd + u_last, last_end), 2);
+            {   // warp-uniform flow control (see wait_uniform)
+                const int np = gw > 0 ? min(t0 + K - 1, pred_end)
+                                      : (t0 + K - 1 >= Pd ? min(t0 + K - Pd + u_last, last_end) : INT_MIN);
+                const int ns = has_succ_ring ? t0 + K - RS + 1 : INT_MIN;
+                wait_uniform(pp + warp, np, false, cp + warp, ns, false);
             }
-            if (lane == 31 && has_succ_ring) spin_until_geq<false>(cp + warp, t0 + K - RS + 1, 3);
-            __syncwarp();
 #pragma unroll 1
             for (int s = 0; s < K; s += U) {
                 const int tg = t0 + s;
