@@ -281,6 +281,9 @@ struct Partial { float cost; int col; int start; int pad; };
 // so diag/left (column w-1) and up (column w) of one chain sit in opposite banks.
 // The query pair is swapped for odd columns by a free FADD2 operand swizzle (.LO_HI)
 // and the reference pairs are stored in their column's orientation.
+#ifndef SDTW_SLOW_UNROLL
+#define SDTW_SLOW_UNROLL 2
+#endif
 #ifndef SDTW_STATIC_SLOW
 #define SDTW_STATIC_SLOW 0
 #endif
@@ -465,10 +468,10 @@ __device__ __forceinline__ void stage_round(float* stage, const float* __restric
 // Round transition of chain c (slow path, rotation offset 0): new strip (y from
 // the staged copy), virtual row -1 = 0, and S(-1, j) = j+1 so that row 0 gets S = j.
 template <int C, int WC, bool TRACE>
-__device__ __forceinline__ void enter_strip(RotRow<C, WC, TRACE>& row, Ys<C, WC>& Y, int c, long strip, bool live,
+__device__ __forceinline__ void enter_strip(RotRow<C, WC, TRACE>& row, Ys<C, WC>& Y, int c, long strip,
                                             const float* ystage, LaneScalars<C>& ls, int off = 0) {
 #pragma unroll
-    for (int w = 0; w < WC; ++w) Y.set(c, w, live ? ystage[w] : INFINITY);
+    for (int w = 0; w < WC; ++w) Y.set(c, w, ystage[w]);
     row.set_all(c, 0.0f, off);
     if constexpr (TRACE) {
 #pragma unroll
@@ -500,18 +503,18 @@ __device__ __forceinline__ void fold_last_row(const RotRow<C, WC, TRACE>& row, i
     }
 }
 
-// Move the row from rotation offset 1 back to offset 0 (slow path only).
-template <int C, int WC, bool TRACE>
-__device__ __forceinline__ void unrotate1(RotRow<C, WC, TRACE>& R) {
+// Move the row from rotation offset SH back to offset 0 (slow path only).
+template <int SH, int C, int WC, bool TRACE>
+__device__ __forceinline__ void unrotate(RotRow<C, WC, TRACE>& R) {
     using RR = RotRow<C, WC, TRACE>;
     RotRow<C, WC, TRACE> T;
 #pragma unroll
     for (int w = 0; w < RR::U; ++w) {
 #pragma unroll
-        for (int p = 0; p < RR::NP; ++p) T.D[p][w] = R.D[p][RR::slot(w, 1)];
+        for (int p = 0; p < RR::NP; ++p) T.D[p][w] = R.D[p][RR::slot(w, SH)];
         if constexpr (TRACE) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) T.S[c][w] = R.S[c][RR::slot(w, 1)];
+            for (int c = 0; c < C; ++c) T.S[c][w] = R.S[c][RR::slot(w, SH)];
         }
     }
     R = T;
@@ -699,32 +702,34 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     // One step on the slow path (rotation offset 0 before and after): per-lane round
     // transitions before, and last-row folds after, the step's cells.
     // One step on the slow path at rotation offset H (H+1 after): per-lane round
-    // transitions before, and last-row folds after, the step's cells.
+    // transitions before, and last-row folds after, the step's cells.  Only the two
+    // per-lane event blocks branch; everything else is select/predicated code.
+    // A chain entering a round past the unit's last one (pc >= Pl) reads a stale
+    // staged strip: its cells are never folded nor handed to the boundary ring.
+    const float* ylane = ystage + lane * C * WC;
+    const E* in_w0 = bnd;                                     // warp 0's inbox = the boundary ring
     auto slow_step = [&](auto hc, int t) {
         constexpr int H = decltype(hc)::value;
         float lin = __shfl_up_sync(FULL, ls.right[C - 1], 1);
         int lins = 0;
         if constexpr (TRACE) lins = __shfl_up_sync(FULL, ls.right_s[C - 1], 1);
-        if (lane == 0) {
-            E e;
-            if (gw == 0) {
-                if (p0 >= 1 || pa > 0) e = my_in[r0];
-                else { e.d = INFINITY; if constexpr (TRACE) e.s = 0; }
-            } else {
-                e = my_in[(t - 1) & (RS - 1)];
+        {
+            E e = (gw == 0) ? in_w0[r0] : my_in[(t - 1) & (RS - 1)];
+            const bool inf_in = gw == 0 && p0 < 1 && pa == 0;    // first round of the first segment
+            if (lane == 0) {
+                lin = inf_in ? INFINITY : e.d;
+                if constexpr (TRACE) lins = inf_in ? 0 : e.s;
             }
-            lin = e.d;
-            if constexpr (TRACE) lins = e.s;
         }
         int rcs[C], pcs[C];                      // chain c is at row r0-c of round pc
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             rcs[c] = (r0 >= c) ? r0 - c : r0 - c + Pd;
             pcs[c] = (r0 >= c) ? p0 : p0 - 1;
-            if (rcs[c] == 0)
-                enter_strip<C, WC, TRACE>(R, Y, c, (long)(pa + pcs[c]) * V + u0 + c, pcs[c] < Pl,
-                                          ystage + (lane * C + c) * WC, ls, H);
         }
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            if (rcs[c] == 0) enter_strip<C, WC, TRACE>(R, Y, c, (long)(pa + pcs[c]) * V + u0 + c, ylane + c * WC, ls, H);
         const XRow<C> x = load_xrow<C>(xs, r0, Pd);
         row_cells<C, WC, FMA, TRACE, H>(R, Y, x, lin, lins, ls);
 #pragma unroll
@@ -733,20 +738,16 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                 fold_last_row<C, WC, TRACE>(R, c, (int)(((long)(pa + pcs[c]) * V + u0 + c) * WC), best[c],
                                             bestcol[c], beststart[c], H + 1);
         }
-        if (lane == 31) {
-            E e;
-            e.d = ls.right[C - 1];
-            if constexpr (TRACE) e.s = ls.right_s[C - 1];
-            if (has_succ_ring) {
-                succ_ring[t & (RS - 1)] = e;
-            } else {
-                const int bl = b0 - (C - 1);               // band of the last chain, row rcs[C-1]
-                if (bl >= 0 && bl < Mtot_bands) succ_ring[rcs[C - 1]] = e;
-            }
+        {
+            E o;
+            o.d = ls.right[C - 1];
+            if constexpr (TRACE) o.s = ls.right_s[C - 1];
+            const int bl = b0 - (C - 1);                 // band of the last chain, row rcs[C-1]
+            E* dst = has_succ_ring ? succ_ring + (t & (RS - 1)) : succ_ring + rcs[C - 1];
+            if (lane == 31 && (has_succ_ring || (bl >= 0 && bl < Mtot_bands))) *dst = o;
         }
         ++b0;
         if (++r0 == Pd) { r0 = 0; ++p0; }
-        __syncwarp();                                   // reconverge before the next step's SHFL
     };
 
     // Warp-uniform period bookkeeping, kept incrementally (no integer division in the
@@ -834,12 +835,21 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                 }
 #if SDTW_STATIC_SLOW
                 // unrolled with compile-time rotation (no register moves)
-                static_for<0, U>([&](auto hc) { slow_step(hc, tg + decltype(hc)::value); });
+                static_for<0, U>([&](auto hc) {
+                    slow_step(hc, tg + decltype(hc)::value);
+                    __syncwarp();
+                });
 #else
+                // SK steps with compile-time rotation per iteration, then one register
+                // shuffle back to offset 0 (SK divides U)
+                constexpr int SK = (SDTW_SLOW_UNROLL < U) ? SDTW_SLOW_UNROLL : U;
 #pragma unroll 1
-                for (int h = 0; h < U; ++h) {
-                    slow_step(std::integral_constant<int, 0>{}, tg + h);
-                    unrotate1<C, WC, TRACE>(R);
+                for (int h = 0; h < U; h += SK) {
+                    static_for<0, SK>([&](auto hc) {
+                        slow_step(hc, tg + h + decltype(hc)::value);
+                        __syncwarp();                    // reconverge before the next step's SHFL
+                    });
+                    unrotate<SK, C, WC, TRACE>(R);
                 }
 #endif
                 reset_xb();
