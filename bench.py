@@ -48,6 +48,20 @@ def gsps(floats: float, ms: float) -> float:
     return floats / (ms * 1e9 / 1000.0)
 
 
+def _traffic(config, w):
+    """DRAM bytes (read + write) per DP launch from the committed ncu capture of this
+    workload (profiles/traffic_<config>.json, written by scripts/ncu_traffic.py from
+    `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum`), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_%s.json" % config)) as f:
+            t = json.load(f)
+        if int(t["Z"]) == int(w["Z_local"]) and int(t["N"]) == w["N"] and int(t["M"]) == w["M"]:
+            return float(t["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -267,7 +281,7 @@ def main():
     achieved = float(w["Z_local"]) * N * M / (dp_avg / 1e3) / 1e9
     clocks = sampler.summary()
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "GCUPS", "frac": achieved / peak,
-            "traffic": None, "sass_per_cell": k, "peak_source": "%s sm_max_mhz=%.0f x %d SMs x %d lanes / %g"
+            "traffic": _traffic(args.config, w), "sass_per_cell": k, "peak_source": "%s sm_max_mhz=%.0f x %d SMs x %d lanes / %g"
             % (src, fmax, sms, LANES_PER_SM, k),
             "headline_peak_k3": peak3, "headline_frac_k3": achieved / peak3,
             "dp_kernel_ms": dp_avg}
@@ -284,13 +298,17 @@ def main():
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
-            t0 = time.perf_counter()
+            # device-timed like the main number: the library enqueues the pinned-host
+            # H2D copy, the kernels and the D2H result copy on this stream
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             if world > 1:
                 distributed_batch(Qh.numpy(), traceback=trace, pre_sharded=True, device=dev)
             else:
                 (sd.traceback if trace else sd.batch)(Qh.numpy())
+            e1.record(stream)
             torch.cuda.synchronize()
-            ts.append(time.perf_counter() - t0)
+            ts.append(e0.elapsed_time(e1) / 1e3)
         te = sum(ts)
         if world > 1:
             t = torch.tensor([te], dtype=torch.float64, device=dev)
