@@ -16,6 +16,7 @@
 #include <mutex>
 #include <string>
 #include <algorithm>
+#include <vector>
 
 namespace {
 
@@ -51,6 +52,8 @@ struct Ctx {
     unsigned char* ws_out = nullptr; size_t ws_out_n = 0;
     double* ws_part = nullptr;                      // reference partial sums + stats
     unsigned char* ws_sched = nullptr; size_t ws_sched_n = 0;   // persistent scheduling state
+    int* order_d = nullptr; size_t order_n = 0;     // unit grab order (device) and its key
+    int64_t order_key[3] = {-1, -1, -1};
     int* flag_d = nullptr;
     int* flag_h = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -196,7 +199,11 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
         }
         const int per_sm = o.workers > 0 ? std::min(o.workers, occ)
                                          : (int)std::max<int64_t>(1, std::min<int64_t>(occ, units / ctx.sms));
-        int S = o.segments > 0 ? o.segments : (int)std::max<int64_t>(1, std::min<int64_t>(16, Pr / 4));
+        // round-segments per ring: enough units to fill the last wave, long enough that the
+        // per-unit fill/drain (~V steps) stays small (r01 sweep: 10M S=32 > 16 > 8; 1M S=16;
+        // 100K S=6 > 8)
+        int S = o.segments > 0 ? o.segments
+                               : (int)std::min<int64_t>(32, std::max<int64_t>(Pr / 16, std::max<int64_t>(1, std::min<int64_t>(16, Pr / 4))));
         if (S > Pr) S = (int)Pr;
         cfg->persistent = 1;
         cfg->S = S;
@@ -225,6 +232,36 @@ sdtw_status launch_dp(const LaunchCfg& c, bool fma, bool trace, const DpParams& 
     CK(cudaLaunchKernelEx(&lc, k, p));
     g_launches++;
     return SDTW_OK;
+}
+
+// Grab order of the persistent units u = seg*R + q (R rings, S round-segments each,
+// W resident workers).  Segments of one ring are sequential (segment s starts from
+// segment s-1's boundary column), so a fixed seg-major order makes a worker that grabs
+// (q, s) while (q, s-1) is still running wait for it -- a whole unit when R is not a
+// multiple of W.  Instead simulate list scheduling with equal unit durations, one wave
+// of W units at a time, longest remaining chain first: every unit is grabbed one wave
+// after its predecessor, and every wave is as full as the chains allow.
+std::vector<int> unit_order(int64_t R, int S, int64_t W) {
+    std::vector<int> order;
+    order.reserve((size_t)(R * S));
+    std::vector<int> next(R, 0);
+    std::vector<int64_t> idx(R);
+    for (int64_t q = 0; q < R; ++q) idx[q] = q;
+    int64_t left = R * S;
+    while (left > 0) {
+        // chains with the most segments left first (stable: lower q on ties)
+        std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return next[a] < next[b]; });
+        int64_t taken = 0;
+        for (int64_t k = 0; k < R && taken < W; ++k) {
+            const int64_t q = idx[k];
+            if (next[q] >= S) continue;
+            order.push_back((int)((int64_t)next[q] * R + q));
+            ++next[q];
+            ++taken;
+            --left;
+        }
+    }
+    return order;
 }
 
 sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
@@ -306,6 +343,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.persistent = cfg.persistent;
     p.S = cfg.S;
     p.counter = nullptr;
+    p.order = nullptr;
     p.seg_done = nullptr;
     p.bnd_g = nullptr;
     p.cand = nullptr;
@@ -322,6 +360,21 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         p.cand = b + 256 + done_b;
         p.bnd_g = static_cast<unsigned char*>(p.cand) + 16 * (size_t)Z * cfg.S;
         CK(cudaMemsetAsync(b, 0, 256 + done_b, st));
+        if (ctx->order_key[0] != (int64_t)R || ctx->order_key[1] != cfg.S || ctx->order_key[2] != cfg.workers) {
+            const std::vector<int> ord = unit_order((int64_t)R, cfg.S, cfg.workers);
+            if (ord.size() > ctx->order_n) {
+                if (ctx->order_d) cudaFree(ctx->order_d);
+                ctx->order_d = nullptr;
+                ctx->order_n = 0;
+                CK(cudaMalloc(&ctx->order_d, ord.size() * sizeof(int)));
+                ctx->order_n = ord.size();
+            }
+            CK(cudaMemcpy(ctx->order_d, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice));
+            ctx->order_key[0] = (int64_t)R;
+            ctx->order_key[1] = cfg.S;
+            ctx->order_key[2] = cfg.workers;
+        }
+        p.order = ctx->order_d;
     }
     if (o.profile) CK(cudaEventRecord(ctx->ev0, st));
     s = launch_dp(cfg, o.fma != 0, trace, p, st);
@@ -520,6 +573,7 @@ void sdtw_release(void) {
     cudaFree(c.ws_out);
     cudaFree(c.ws_part);
     cudaFree(c.ws_sched);
+    cudaFree(c.order_d);
     cudaFree(c.flag_d);
     cudaFreeHost(c.flag_h);
     cudaEventDestroy(c.ev0);

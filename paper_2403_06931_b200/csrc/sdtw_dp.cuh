@@ -64,6 +64,7 @@ struct DpParams {
     int S;
     int Zq;                // real number of queries (dual-query kernel: P.Z counts pairs)
     int* counter;
+    const int* order;      // grab order of the units (nullptr = identity), see unit_order() in sdtw_api.cu
     int* seg_done;
     void* bnd_g;
     void* cand;
@@ -599,7 +600,10 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     // ---- which unit: (query q, rounds [pa, pb))
     int q, seg = 0, pa = 0, pb = P.Pr;
     if (P.persistent) {
-        if (threadIdx.x == 0) *unit_sh = atomicAdd(P.counter, 1);
+        if (threadIdx.x == 0) {
+            const int raw = atomicAdd(P.counter, 1);
+            *unit_sh = (P.order && raw < P.Z * P.S) ? P.order[raw] : raw;
+        }
         __syncthreads();
         const int u = *unit_sh;
         __syncthreads();

@@ -209,7 +209,10 @@ __global__ void __launch_bounds__(384) sdtw_dpq_kernel(const DpParams P) {
         // ---- which unit: (query pair qp, rounds [pa, pb))
         int qp, seg = 0, pa = 0, pb = P.Pr;
         if (P.persistent) {
-            if (threadIdx.x == 0) *unit_sh = atomicAdd(P.counter, 1);
+            if (threadIdx.x == 0) {
+                const int raw = atomicAdd(P.counter, 1);
+                *unit_sh = (P.order && raw < P.Z * P.S) ? P.order[raw] : raw;
+            }
             __syncthreads();
             const int u = *unit_sh;
             __syncthreads();
