@@ -40,6 +40,11 @@
 #include <cuda_runtime.h>
 #include <type_traits>
 
+// Build-time knobs (A/B variants via -D; the defaults are the measured best)
+#ifndef SDTW_SPIN_NS
+#define SDTW_SPIN_NS 256         // nanosleep per flow-control poll (r01 A/B: 256 > 64 by 0.8 %)
+#endif
+
 namespace sdtw {
 namespace cg = cooperative_groups;
 
@@ -159,7 +164,7 @@ __device__ __forceinline__ int ld_acquire_hop(const int* p, bool remote) {
 // Waits until (*pa >= na || na == INT_MIN) && (*pb >= nb || nb == INT_MIN).
 static __device__ __noinline__ void wait_uniform_slow(const int* pa, int na, bool ra, const int* pb, int nb, bool rb) {
     for (long long n = 0;; ++n) {
-        __nanosleep(64);
+        __nanosleep(SDTW_SPIN_NS);
         bool ok = true;
         if (na != INT_MIN) ok = ld_acquire_hop(pa, ra) >= na;
         if (nb != INT_MIN) ok = ok && ld_acquire_hop(pb, rb) >= nb;
@@ -289,10 +294,20 @@ struct Partial { float cost; int col; int start; int pad; };
 #define SDTW_STATIC_SLOW 0
 #endif
 #ifndef SDTW_ALT_ORIENT
-#define SDTW_ALT_ORIENT 1
+#define SDTW_ALT_ORIENT 2
 #endif
-__host__ __device__ __forceinline__ constexpr int pair_half(int c, int w) {   // half of chain c at column w
+__host__ __device__ __forceinline__ constexpr int pair_half(int c, int w) {   // reference pairs: half of chain c at column w
     return SDTW_ALT_ORIENT ? ((c ^ w) & 1) : (c & 1);
+}
+// Row values: half of chain c at column w when the row sits at rotation offset off.
+// Mode 2 ("diagonal" orientation, the default) flips it with the offset as well: a
+// cell's new value then has the orientation of its diag input, so the two FMNMX3 of a
+// pair can write their minima straight into the dead diag register pair and FFMA2 works
+// in place -- no register copies at the end of a rotation period -- while diag/up of
+// one chain still sit in opposite banks.  Needs even rotation periods and slow-step
+// groups (U and SDTW_SLOW_UNROLL even).
+__host__ __device__ __forceinline__ constexpr int orient(int c, int w, int off) {
+    return SDTW_ALT_ORIENT == 2 ? ((c ^ w ^ off) & 1) : pair_half(c, w);
 }
 __device__ __forceinline__ float half_of(unsigned long long r, int h) { return h ? hi32(r) : lo32(r); }
 __device__ __forceinline__ unsigned long long with_half(unsigned long long r, int h, float v) {
@@ -307,18 +322,18 @@ template <int C, int WC, bool TRACE> struct RotRow {
     __device__ __forceinline__ static constexpr int slot(int w, int h) { return ((w - h) % U + U) % U; }
     __device__ __forceinline__ float d(int c, int w) const {   // offset 0: slot w holds column w
         if constexpr (C == 1) return D[0][w];
-        else return half_of(D[c >> 1][w], pair_half(c, w));
+        else return half_of(D[c >> 1][w], orient(c, w, 0));
     }
     __device__ __forceinline__ float d_at(int c, int w, int off) const {   // rotation offset off
         if constexpr (C == 1) return D[0][slot(w, off)];
-        else return half_of(D[c >> 1][slot(w, off)], pair_half(c, w));
+        else return half_of(D[c >> 1][slot(w, off)], orient(c, w, off));
     }
     __device__ __forceinline__ int s_at(int c, int w, int off) const { return S[TRACE ? c : 0][TRACE ? slot(w, off) : 0]; }
     __device__ __forceinline__ void set_all(int c, float v, int off = 0) {  // every slot of chain c
 #pragma unroll
         for (int w = 0; w < U; ++w) {                           // column w lives in slot(w, off)
             if constexpr (C == 1) D[0][slot(w, off)] = v;
-            else D[c >> 1][slot(w, off)] = with_half(D[c >> 1][slot(w, off)], pair_half(c, w), v);
+            else D[c >> 1][slot(w, off)] = with_half(D[c >> 1][slot(w, off)], orient(c, w, off), v);
         }
     }
 };
@@ -413,15 +428,17 @@ __device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, W
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
                 const int c0 = 2 * p, c1 = 2 * p + 1;
-                const int ow = pair_half(0, w), od = pair_half(0, w - 1);   // orientation of columns w, w-1
+                // orientation of old column w (up), old column w-1 (diag), new column w
+                const int ow = orient(0, w, H), od = orient(0, w - 1, H), on = orient(0, w, H + 1);
                 const float u0 = half_of(R.D[p][ku], ow), u1 = half_of(R.D[p][ku], ow ^ 1);
                 const float d0 = (w == 0) ? pd[c0] : half_of(R.D[p][kd], od);
                 const float d1 = (w == 0) ? pd[c1] : half_of(R.D[p][kd], od ^ 1);
                 const float m0 = min3f(d0, u0, left[c0]);
                 const float m1 = min3f(d1, u1, left[c1]);
-                const unsigned long long xw = ow ? pk(hi32(x.p[p]), lo32(x.p[p])) : x.p[p];   // FADD2 .LO_HI
-                const unsigned long long vv = ow ? cell2<FMA>(xw, Y.Y[p][w], m1, m0)
-                                                 : cell2<FMA>(xw, Y.Y[p][w], m0, m1);
+                // operand swaps fold into FADD2 swizzles (.LO_HI)
+                const unsigned long long xw = on ? pk(hi32(x.p[p]), lo32(x.p[p])) : x.p[p];
+                const unsigned long long yw = (pair_half(0, w) != on) ? pk(hi32(Y.Y[p][w]), lo32(Y.Y[p][w])) : Y.Y[p][w];
+                const unsigned long long vv = on ? cell2<FMA>(xw, yw, m1, m0) : cell2<FMA>(xw, yw, m0, m1);
                 if constexpr (TRACE) {
                     const int su0 = R.S[c0][ku], su1 = R.S[c1][ku];
                     const int sd0 = (w == 0) ? psd[c0] : R.S[c0][kd];
@@ -434,8 +451,8 @@ __device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, W
                     sl[c1] = sv1;
                 }
                 R.D[p][kd] = vv;
-                left[c0] = half_of(vv, ow);
-                left[c1] = half_of(vv, ow ^ 1);
+                left[c0] = half_of(vv, on);
+                left[c1] = half_of(vv, on ^ 1);
             }
         }
     }
@@ -847,6 +864,8 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                 // SK steps with compile-time rotation per iteration, then one register
                 // shuffle back to offset 0 (SK divides U)
                 constexpr int SK = (SDTW_SLOW_UNROLL < U) ? SDTW_SLOW_UNROLL : U;
+                static_assert(SDTW_ALT_ORIENT != 2 || C == 1 || (SK % 2 == 0 && U % 2 == 0),
+                              "diagonal orientation needs even rotation groups");
 #pragma unroll 1
                 for (int h = 0; h < U; h += SK) {
                     static_for<0, SK>([&](auto hc) {
