@@ -169,7 +169,8 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // chunk: 64 steps when the query is long enough that the round period stays N
     // (Pd >= V + (G+1)K), else 32 (r01 sweep: K=64 +1.5% over 32, K=128 -12%)
     const int Kreq = o.chunk > 0 ? o.chunk : (N >= V + (int64_t)(G + 1) * 64 ? 64 : 32);
-    const int K = U * std::max(1, (Kreq + U / 2) / U);
+    const int KU = (dual ? 1 : SDTW_FAST_PERIODS) * U;   // chunk = whole fast/slow decision windows
+    const int K = KU * std::max(1, (Kreq + KU / 2) / KU);
     const int64_t need = V + (int64_t)(G + 1) * K;
     const int64_t Pd = N > need ? N : need;
     const int64_t Pr = (ctx.M + V * WC - 1) / (V * WC);

@@ -287,6 +287,9 @@ struct Partial { float cost; int col; int start; int pad; };
 // so diag/left (column w-1) and up (column w) of one chain sit in opposite banks.
 // The query pair is swapped for odd columns by a free FADD2 operand swizzle (.LO_HI)
 // and the reference pairs are stored in their column's orientation.
+#ifndef SDTW_FAST_PERIODS
+#define SDTW_FAST_PERIODS 1
+#endif
 #ifndef SDTW_SLOW_UNROLL
 #define SDTW_SLOW_UNROLL 2
 #endif
@@ -559,6 +562,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
     using E = Entry<TRACE>;
     using RowT = RotRow<C, WC, TRACE>;
     constexpr int U = RowT::U;
+    constexpr int PS = SDTW_FAST_PERIODS * U;        // steps per fast/slow decision (K % PS == 0)
 
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = CLUSTER ? (int)cluster.num_blocks() : 1;
@@ -798,13 +802,14 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
             wait_uniform(pp + warp, np, pred_remote, cp + warp, ns, succ_remote);
         }
 
-        // ---- per rotation period (U steps): "fast" when no lane of this warp crosses
+        // ---- per PS = SDTW_FAST_PERIODS rotation periods (U steps each): "fast" when no
+        // lane of this warp crosses
         // row 0 (round transition) or row N-1 (last-row fold) inside it ->
         // warp-uniform, branch-free steps; otherwise U per-lane slow steps.
 #pragma unroll 1
-        for (int s = 0; s < K; s += U) {
+        for (int s = 0; s < K; s += PS) {
             const int tg = t0 + s;
-            const int lo = rw - (32 * C - 1), hi = rw + U - 1;
+            const int lo = rw - (32 * C - 1), hi = rw + PS - 1;
             const bool hit0 = lo <= 0 || hi >= Pd;
             const bool hitN = (lo <= Nm1 && Nm1 <= hi) || lo <= Nm1 - Pd || Nm1 + Pd <= hi;
             if (!hit0 && !hitN) {
@@ -824,7 +829,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                     ib1 = my_in + (tg & (RS - 1));
                 }
                 E* ob = has_succ_ring ? succ_ring + (tg & (RS - 1)) : succ_ring + lo;
-                static_for<0, U>([&](auto hc) {
+                static_for<0, PS>([&](auto hc) {
                     constexpr int h = decltype(hc)::value;
                     float lin = __shfl_up_sync(FULL, ls.right[C - 1], 1);
                     int lins = 0;
@@ -835,7 +840,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                         if constexpr (TRACE) lins = e.s;
                     }
                     const XRow<C> x = load_xrow_fast<C, h>(xb);
-                    row_cells<C, WC, FMA, TRACE, h>(R, Y, x, lin, lins, ls);
+                    row_cells<C, WC, FMA, TRACE, h % U>(R, Y, x, lin, lins, ls);
                     if (lane == 31) {
                         E o;
                         o.d = ls.right[C - 1];
@@ -843,11 +848,11 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                         ob[h] = o;
                     }
                 });
-                b0 += U;
-                r0 += U;                                     // may land exactly on the next round
+                b0 += PS;
+                r0 += PS;                                    // may land exactly on the next round
                 if (r0 >= Pd) { r0 -= Pd; ++p0; }
 #pragma unroll
-                for (int j = 0; j < NC; ++j) xb[j] += (U / NC) * XC;   // rows r0+j keep their residue (U % C == 0);
+                for (int j = 0; j < NC; ++j) xb[j] += (PS / NC) * XC;   // rows r0+j keep their residue (U % C == 0);
                 // a wrap of r0 makes the next period slow, which resets xb
             } else {
                 if (hit0) {                                  // a transition reads the staged strips
@@ -856,8 +861,8 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                 }
 #if SDTW_STATIC_SLOW
                 // unrolled with compile-time rotation (no register moves)
-                static_for<0, U>([&](auto hc) {
-                    slow_step(hc, tg + decltype(hc)::value);
+                static_for<0, PS>([&](auto hc) {
+                    slow_step(std::integral_constant<int, decltype(hc)::value % U>{}, tg + decltype(hc)::value);
                     __syncwarp();
                 });
 #else
@@ -867,7 +872,7 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
                 static_assert(SDTW_ALT_ORIENT != 2 || C == 1 || (SK % 2 == 0 && U % 2 == 0),
                               "diagonal orientation needs even rotation groups");
 #pragma unroll 1
-                for (int h = 0; h < U; h += SK) {
+                for (int h = 0; h < PS; h += SK) {
                     static_for<0, SK>([&](auto hc) {
                         slow_step(hc, tg + h + decltype(hc)::value);
                         __syncwarp();                    // reconverge before the next step's SHFL
@@ -877,10 +882,10 @@ __global__ void __launch_bounds__(256) sdtw_dp_kernel(const DpParams P) {
 #endif
                 reset_xb();
             }
-            rw += U;
+            rw += PS;
             if (rw >= Pd) { rw -= Pd; ++pw; }
             // the last lane of this warp has entered round pf_round: stage round pf_round+1
-            if (tg + U > stage_t && pf_round + 1 < Pl) {
+            if (tg + PS > stage_t && pf_round + 1 < Pl) {
                 ++pf_round;
                 stage_t += Pd;
                 __syncwarp();
