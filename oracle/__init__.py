@@ -42,6 +42,8 @@ def lib():
         L.oracle_sdtw_full.restype = ctypes.c_int
         L.oracle_walkback.argtypes = [f32p, i64, i64, i64]
         L.oracle_walkback.restype = i64
+        L.oracle_walkback_path.argtypes = [f32p, i64, i64, i64, i64p, i64p]
+        L.oracle_walkback_path.restype = ctypes.c_int
         L.oracle_znorm.argtypes = [f32p, i64, i64, f32p]
         L.oracle_znorm.restype = ctypes.c_int
         _lib = L
@@ -103,6 +105,28 @@ def walkback(D, end: int) -> int:
     Dc, dp = _f32(D)
     N, M = Dc.shape
     return int(lib().oracle_walkback(dp, N, M, int(end)))
+
+
+def walkback_path(D, end: int):
+    """Full warp path of the walk-back from (N-1, end): per row i the first and last
+    column visited, (lo[N], hi[N]) int64."""
+    Dc, dp = _f32(D)
+    N, M = Dc.shape
+    lo = np.empty(N, np.int64)
+    hi = np.empty(N, np.int64)
+    if lib().oracle_walkback_path(dp, N, M, int(end), _i64(lo), _i64(hi)) != 0:
+        raise ValueError("oracle_walkback_path: bad arguments")
+    return lo, hi
+
+
+def sdtw_path(x, Y, fma: bool = True):
+    """(cost, end, start, lo, hi) of one query from the full matrices -- small instances."""
+    D, S = sdtw_full(x, Y, fma)
+    last = D[-1]
+    cost = last.min()
+    end = int(np.flatnonzero(last == cost)[0])
+    lo, hi = walkback_path(D, end)
+    return np.float32(cost), end, int(S[-1, end]), lo, hi
 
 
 def znorm(X):

@@ -201,6 +201,29 @@ int64_t oracle_walkback(const float* D, int64_t N, int64_t M, int64_t end)
     return j;
 }
 
+/* The full warp path: the cells the paper's walk-back
+ * visits from (N-1, end) down to row 0, with the same neighbour order and tie rule
+ * as oracle_walkback.  A monotone path visits a contiguous run of columns in each
+ * row, so the path is reported as lo[i] <= hi[i], the first and last column it
+ * visits in row i (lo[0] is the start column).  Returns 0, or 1 on bad arguments. */
+int oracle_walkback_path(const float* D, int64_t N, int64_t M, int64_t end, int64_t* lo, int64_t* hi)
+{
+    if (N < 1 || M < 1 || end < 0 || end >= M) return 1;
+    int64_t i = N - 1, j = end;
+    lo[i] = hi[i] = j;
+    while (i > 0) {
+        float diag = (j > 0) ? D[(i - 1) * M + j - 1] : ORACLE_INF;
+        float up = D[(i - 1) * M + j];
+        float left = (j > 0) ? D[i * M + j - 1] : ORACLE_INF;
+        float m = min3(diag, up, left);
+        if (diag == m && j > 0) { i -= 1; j -= 1; hi[i] = j; }
+        else if (up == m) { i -= 1; hi[i] = j; }
+        else { j -= 1; }
+        lo[i] = j;
+    }
+    return 0;
+}
+
 /* z-normalisation of n_series contiguous series of length len (Eq. 2). */
 int oracle_znorm(const float* in, int64_t n_series, int64_t len, float* out)
 {
