@@ -86,6 +86,22 @@ sdtw_status sdtw_batch(const float* Q, int64_t n_queries, int64_t N,
 sdtw_status sdtw_traceback(const float* Q, int64_t n_queries, int64_t N,
                            float* out_cost, int64_t* out_end, int64_t* out_start);
 
+/* As sdtw_traceback, plus the full optimal warp path of every query (SURVEY.md
+ * §8(f) NEXT-2; the walk-back of P:L35 from (N-1, out_end) with the tie rule
+ * diag > up > left).  A monotone warp path visits a contiguous run of reference
+ * columns in each query row, so the path is returned as path_lo / path_hi:
+ * n_queries x N int32, row-major; row i of query q covers columns
+ * [path_lo[q*N+i], path_hi[q*N+i]], path_lo[q*N] == out_start[q] and
+ * path_hi[q*N+N-1] == out_end[q]; consecutive rows satisfy
+ * path_lo[i+1] in {path_hi[i], path_hi[i]+1}.  A query whose cost is +inf (raw-mode
+ * overflow) gets -1 everywhere.  Computed by re-running the DP on columns
+ * [start, end] with 2-bit predecessor codes (device workspace <= 1 GiB, queries in
+ * chunks).  Pointers may be host or device (current device).  Errors: as
+ * sdtw_traceback; SDTW_E_NOMEM when one query's window codes exceed the workspace. */
+sdtw_status sdtw_path(const float* Q, int64_t n_queries, int64_t N,
+                      float* out_cost, int64_t* out_end, int64_t* out_start,
+                      int32_t* path_lo, int32_t* path_hi);
+
 /* z-normalisation of n_series contiguous series of length len (the paper's
  * runNormalizer; Eq. 2 P:L73 with the population variance of P:L85-L86):
  * fp64 accumulation, z = fl32((x - mean)/sd); degenerate series (var <= 1e-12 *

@@ -7,7 +7,7 @@ fallback: importing this package fails loudly when the library is missing, and
 every call raises when the CUDA path fails.
 
 Functions mirror the ABI names (minus the ``sdtw_`` prefix):
-``set_reference``, ``batch``, ``traceback``, ``znormalize``, ``set_option``,
+``set_reference``, ``batch``, ``traceback``, ``path``, ``znormalize``, ``set_option``,
 ``get_option``, ``profile``, ``launch_count``, ``release``.
 Inputs may be torch tensors (CUDA or CPU) or numpy arrays.  torch supplies
 device memory and the current stream (passed as SDTW_OPT_STREAM).
@@ -34,6 +34,8 @@ _i64 = ctypes.c_int64
 _lib.sdtw_set_reference.argtypes = [ctypes.c_void_p, _i64]
 _lib.sdtw_batch.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p]
 _lib.sdtw_traceback.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+_lib.sdtw_path.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_void_p]
 _lib.sdtw_znormalize.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p]
 _lib.sdtw_set_option.argtypes = [ctypes.c_int, _i64]
 _lib.sdtw_get_option.argtypes = [ctypes.c_int, ctypes.POINTER(_i64)]
@@ -41,7 +43,7 @@ _lib.sdtw_profile.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i
 _lib.sdtw_launch_count.restype = _i64
 _lib.sdtw_last_error.restype = ctypes.c_char_p
 _lib.sdtw_version.restype = ctypes.c_int
-for _n in ("sdtw_set_reference", "sdtw_batch", "sdtw_traceback", "sdtw_znormalize",
+for _n in ("sdtw_set_reference", "sdtw_batch", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
            "sdtw_set_option", "sdtw_get_option", "sdtw_profile"):
     getattr(_lib, _n).restype = ctypes.c_int
 
@@ -52,7 +54,7 @@ OPT_NORMALIZE, OPT_FMA, OPT_SEGMENT_W, OPT_LANES, OPT_CLUSTER, OPT_STREAM, OPT_P
 _STATUS = {0: "SDTW_OK", 1: "SDTW_E_ARG", 2: "SDTW_E_NOREF", 3: "SDTW_E_CUDA", 4: "SDTW_E_NOMEM",
            5: "SDTW_E_NONFINITE"}
 
-EXPORTED_SYMBOLS = ("sdtw_set_reference", "sdtw_batch", "sdtw_traceback", "sdtw_znormalize",
+EXPORTED_SYMBOLS = ("sdtw_set_reference", "sdtw_batch", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
                     "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_launch_count",
                     "sdtw_last_error", "sdtw_release", "sdtw_version")
 
@@ -160,6 +162,29 @@ def traceback(Q):
     _check(_lib.sdtw_traceback(ctypes.c_void_p(ptr), Z, N, ctypes.c_void_p(pc), ctypes.c_void_p(pe),
                                ctypes.c_void_p(ps)))
     return cost, end, start
+
+
+def path(Q):
+    """sdtw_path: Q [Z, N] -> (cost, end, start, path_lo [Z, N] int32, path_hi [Z, N] int32):
+    row i of query q's optimal warp path covers reference columns path_lo[q, i]..path_hi[q, i]."""
+    keep, ptr, shape = _as_f32(Q)
+    if len(shape) == 1:
+        shape = (1, shape[0])
+    Z, N = shape
+    cost, end, start, (pc, pe, ps) = _outputs(keep, Z, True)
+    torch = _torch()
+    if torch is not None and isinstance(keep, torch.Tensor) and keep.is_cuda:
+        lo = torch.empty((Z, N), dtype=torch.int32, device=keep.device)
+        hi = torch.empty((Z, N), dtype=torch.int32, device=keep.device)
+        pl, ph = lo.data_ptr(), hi.data_ptr()
+    else:
+        lo = np.empty((Z, N), np.int32)
+        hi = np.empty((Z, N), np.int32)
+        pl, ph = lo.ctypes.data, hi.ctypes.data
+    _bind_stream(keep)
+    _check(_lib.sdtw_path(ctypes.c_void_p(ptr), Z, N, ctypes.c_void_p(pc), ctypes.c_void_p(pe),
+                          ctypes.c_void_p(ps), ctypes.c_void_p(pl), ctypes.c_void_p(ph)))
+    return cost, end, start, lo, hi
 
 
 def znormalize(X):

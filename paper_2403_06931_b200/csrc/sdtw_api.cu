@@ -8,6 +8,7 @@
 #include "sdtw_dp.cuh"
 #include "sdtw_dp_pick.h"
 #include "sdtw_dpq.cuh"
+#include "sdtw_path.cuh"
 #include "sdtw_prep.cuh"
 
 #include <atomic>
@@ -52,6 +53,7 @@ struct Ctx {
     unsigned char* ws_out = nullptr; size_t ws_out_n = 0;
     double* ws_part = nullptr;                      // reference partial sums + stats
     unsigned char* ws_sched = nullptr; size_t ws_sched_n = 0;   // persistent scheduling state
+    unsigned char* ws_path = nullptr; size_t ws_path_n = 0;     // sdtw_path codes / row buffers / outputs
     int* order_d = nullptr; size_t order_n = 0;     // unit grab order (device) and its key
     int64_t order_key[3] = {-1, -1, -1};
     int* flag_d = nullptr;
@@ -265,8 +267,17 @@ std::vector<int> unit_order(int64_t R, int S, int64_t W) {
     return order;
 }
 
+// Device-side views of a finished batch (for sdtw_path): the query samples the DP
+// used and the per-query results, valid until the next call.
+struct BatchDev {
+    const float* x = nullptr;
+    const float* cost = nullptr;
+    const int64_t* end = nullptr;
+    const int64_t* start = nullptr;
+};
+
 sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
-                      int64_t* out_start, bool trace) {
+                      int64_t* out_start, bool trace, BatchDev* dev_out = nullptr) {
     if (N < 1 || Z < 0) return fail(SDTW_E_ARG, "N must be >= 1 and n_queries >= 0");
     if (Z > 0 && (!Q || !out_cost || !out_end || (trace && !out_start)))
         return fail(SDTW_E_ARG, "NULL pointer");
@@ -396,6 +407,12 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     }
     ctx->last_launches = g_launches.load() - launches0;
     if (*ctx->flag_h) return fail(SDTW_E_NONFINITE, "query batch contains a non-finite sample");
+    if (dev_out) {
+        dev_out->x = xd;
+        dev_out->cost = dc;
+        dev_out->end = de;
+        dev_out->start = ds;
+    }
     if (host_out) {
         // copy each output to wherever it lives
         auto cp = [&](void* dst, const void* src, size_t bytes, int kind) -> cudaError_t {
@@ -406,6 +423,88 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         if (trace && ds != out_start) CK(cp(out_start, ds, Z * sizeof(int64_t), ks));
         CK(cudaStreamSynchronize(st));
     }
+    return SDTW_OK;
+}
+
+// sdtw_path: the batch with start propagation, then per query the window DP with
+// predecessor codes and the walk-back (sdtw_path.cuh), in chunks of queries whose codes
+// fit the workspace budget.
+constexpr size_t kPathBudget = size_t(1) << 30;
+
+sdtw_status run_path(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
+                     int64_t* out_start, int32_t* path_lo, int32_t* path_hi) {
+    if (Z > 0 && (!path_lo || !path_hi)) return fail(SDTW_E_ARG, "NULL pointer");
+    BatchDev bd;
+    sdtw_status s = run_batch(Q, Z, N, out_cost, out_end, out_start, true, &bd);
+    if (s != SDTW_OK || Z == 0) return s;
+    Ctx* ctx;
+    s = get_ctx(&ctx);
+    if (s != SDTW_OK) return s;
+    const Options o = g_opt;
+    cudaStream_t st = o.stream;
+    const int kl = ptr_kind(path_lo), kh = ptr_kind(path_hi);
+    if (kl < 0 || kh < 0) return fail(SDTW_E_ARG, "device pointer on another device");
+    // window widths (host): one small D2H of the per-query results
+    std::vector<int64_t> hs(Z), he(Z);
+    std::vector<float> hc(Z);
+    CK(cudaMemcpyAsync(hs.data(), bd.start, Z * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(he.data(), bd.end, Z * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc.data(), bd.cost, Z * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int64_t Lmax = 1;
+    for (int64_t q = 0; q < Z; ++q)
+        if (hc[q] < INFINITY) Lmax = std::max<int64_t>(Lmax, he[q] - hs[q] + 1);
+    const int64_t W = (Lmax + 15) / 16;
+    const bool stage_out = (kl == 0 || kh == 0);
+    const size_t per_q = (size_t)N * W * 4 + (size_t)Lmax * 4 + (stage_out ? (size_t)N * 8 : 0);
+    const int64_t chunk = std::min<int64_t>(Z, (int64_t)(kPathBudget / per_q));
+    if (chunk < 1) return fail(SDTW_E_NOMEM, "path window too large for the workspace budget");
+    const size_t need = (size_t)chunk * per_q + 256;
+    if (need > ctx->ws_path_n) {
+        if (ctx->ws_path) cudaFree(ctx->ws_path);
+        ctx->ws_path = nullptr;
+        ctx->ws_path_n = 0;
+        CK(cudaMalloc(&ctx->ws_path, need));
+        ctx->ws_path_n = need;
+    }
+    uint32_t* codes = reinterpret_cast<uint32_t*>(ctx->ws_path);
+    float* rowbuf = reinterpret_cast<float*>(codes + (size_t)chunk * N * W);
+    int32_t* slo = reinterpret_cast<int32_t*>(rowbuf + (size_t)chunk * Lmax);
+    int32_t* shi = slo + (size_t)chunk * N;
+    CK(cudaMemsetAsync(ctx->flag_d, 0, sizeof(int), st));
+    const int T = (int)std::min<int64_t>(256, (N + 31) / 32 * 32);
+    for (int64_t q0 = 0; q0 < Z; q0 += chunk) {
+        const int zc = (int)std::min<int64_t>(chunk, Z - q0);
+        sdtw::PathParams p;
+        p.X = bd.x + q0 * N;
+        p.Y = ctx->ref;
+        p.cost = bd.cost + q0;
+        p.start = bd.start + q0;
+        p.end = bd.end + q0;
+        p.N = (int)N;
+        p.W = (int)W;
+        p.Lmax = (int)Lmax;
+        p.codes = codes;
+        p.rowbuf = rowbuf;
+        p.path_lo = stage_out ? slo : path_lo + q0 * N;
+        p.path_hi = stage_out ? shi : path_hi + q0 * N;
+        p.err_flag = ctx->flag_d;
+        if (o.fma) sdtw::path_dp_kernel<true><<<zc, T, 2 * T * sizeof(float), st>>>(p);
+        else sdtw::path_dp_kernel<false><<<zc, T, 2 * T * sizeof(float), st>>>(p);
+        sdtw::path_walk_kernel<<<(zc + 127) / 128, 128, 0, st>>>(p, zc);
+        CK(cudaGetLastError());
+        g_launches += 2;
+        if (stage_out) {
+            CK(cudaMemcpyAsync(path_lo + q0 * N, slo, (size_t)zc * N * 4,
+                               kl ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(path_hi + q0 * N, shi, (size_t)zc * N * 4,
+                               kh ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+        }
+    }
+    CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (*ctx->flag_h) return fail(SDTW_E_CUDA, "internal: path recomputation did not reproduce the batch result");
+    ctx->last_launches += 2 * ((Z + chunk - 1) / chunk);
     return SDTW_OK;
 }
 
@@ -458,6 +557,12 @@ sdtw_status sdtw_traceback(const float* Q, int64_t n_queries, int64_t N, float* 
                            int64_t* out_start) {
     std::lock_guard<std::mutex> lk(g_mu);
     return run_batch(Q, n_queries, N, out_cost, out_end, out_start, true);
+}
+
+sdtw_status sdtw_path(const float* Q, int64_t n_queries, int64_t N, float* out_cost, int64_t* out_end,
+                      int64_t* out_start, int32_t* path_lo, int32_t* path_hi) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return run_path(Q, n_queries, N, out_cost, out_end, out_start, path_lo, path_hi);
 }
 
 sdtw_status sdtw_znormalize(const float* in, int64_t n_series, int64_t len, float* out) {
@@ -574,6 +679,7 @@ void sdtw_release(void) {
     cudaFree(c.ws_out);
     cudaFree(c.ws_part);
     cudaFree(c.ws_sched);
+    cudaFree(c.ws_path);
     cudaFree(c.order_d);
     cudaFree(c.flag_d);
     cudaFreeHost(c.flag_h);
