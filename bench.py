@@ -202,6 +202,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--path", action="store_true",
+                    help="step = sdtw_path (start index + full warp path, SURVEY NEXT-2); 1 GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -232,9 +234,15 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    if args.path and world > 1:
+        raise SystemExit("--path runs on one GPU")
+    trace = trace or args.path
+
     def step():
         if world > 1:
             return distributed_batch(Qd, traceback=trace, pre_sharded=True, device=dev)
+        if args.path:
+            return sd.path(Qd)
         return sd.traceback(Qd) if trace else sd.batch(Qd)
 
     for _ in range(args.warmup):
@@ -292,7 +300,8 @@ def main():
     e2e = None
     if not args.no_e2e:
         Qh = torch.from_numpy(Q).pin_memory()
-        sd.batch(Qh.numpy()) if not trace else sd.traceback(Qh.numpy())
+        api = sd.path if args.path else (sd.traceback if trace else sd.batch)
+        api(Qh.numpy())
         ts = []
         for i in range(max(1, min(args.steps, 3))):
             torch.cuda.synchronize()
@@ -305,7 +314,7 @@ def main():
             if world > 1:
                 distributed_batch(Qh.numpy(), traceback=trace, pre_sharded=True, device=dev)
             else:
-                (sd.traceback if trace else sd.batch)(Qh.numpy())
+                api(Qh.numpy())
             e1.record(stream)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) / 1e3)
@@ -316,7 +325,7 @@ def main():
             te = float(t.item())
         e2e = {"value": cells_step * len(ts) / te / 1e9, "unit": "GCUPS",
                "h2d_bytes_per_step": int(Q.nbytes) * world,
-               "d2h_bytes_per_step": int(w["Z"]) * (4 + 8 + (8 if trace else 0))}
+               "d2h_bytes_per_step": int(w["Z"]) * (4 + 8 + (8 if trace else 0) + (8 * N if args.path else 0))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -337,6 +346,14 @@ def main():
             "gsps_eq3": gsps(float(w["Z"]) * N, tot_ms / args.steps),
             "e2e": e2e, "cpu_baseline": cpu,
         }
+        if args.path:
+            c, e, st, lo, hi = step()
+            L = (e - st + 1).double()
+            line["path"] = {"window_cells_per_step": float((L * N).sum().item()),
+                            "path_cells_per_step": float((hi - lo + 1).double().sum().item()),
+                            "step_ms_incl_path": tot_ms / args.steps, "dp_kernel_ms": dp_avg,
+                            "non_dp_share": 1.0 - dp_avg / (tot_ms / args.steps)}
+            line["config"]["workload"] += " + full warp path (sdtw_path)"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
