@@ -280,7 +280,8 @@ def main():
     peaks, src = _peaks()
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    packed = sd.get_option(sd.OPT_PACKED) != 0
+    popt = sd.get_option(sd.OPT_PACKED)
+    packed = popt > 0 or (popt < 0 and not trace)          # the library's auto choice (sdtw_api.cu plan)
     mix = ("packed" if packed else "scalar") + "_fma" + ("_trace" if trace else "")
     k = SASS_PER_CELL[mix]
     peak = sms * LANES_PER_SM * fmax * 1e6 / k / 1e9

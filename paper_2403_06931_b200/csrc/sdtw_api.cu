@@ -150,7 +150,10 @@ struct LaunchCfg {
 // chains (C=4), 3 dual-query x 2 chains, 4 dual-query x 1 chain; -1 auto.
 sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cfg) {
     const Options& o = g_opt;
-    const int packed = o.packed < 0 ? 1 : o.packed;
+    // auto: two packed chains (f32x2) for cost/end; scalar strips for the start-index
+    // variant, whose per-cell start selects double the registers per slot (r01 sweep at
+    // N=1000: scalar W=15 3.00, packed W=14 2.89, packed W=30 1.80 TCUPS)
+    const int packed = o.packed < 0 ? (trace ? 0 : 1) : o.packed;
     const bool dual = packed >= 3;
     int C = dual ? (packed == 3 ? 2 : 1) : (packed == 0 ? 1 : (packed == 1 ? 2 : 4));
     int W = o.segment_w > 0 ? o.segment_w : (C == 4 ? 28 : (C == 2 ? 30 : 15));

@@ -226,6 +226,21 @@ __device__ __forceinline__ unsigned long long cell2(unsigned long long xx, unsig
     return vv;
 }
 
+// Start-column select of the TRACE variant, priority diag > up > left on equality
+// (reading G6): branch-free FSETP + SEL pairs (the ternary form compiled to a
+// BSSY/BRA/BSYNC diamond per cell -- 4.3x the instructions of the plain DP).
+__device__ __forceinline__ int start_sel(float d, float u, float m, int sd, int su, int sl) {
+    int r;
+    asm("{\n\t.reg .pred pu, pd;\n\t"
+        "setp.eq.f32 pu, %2, %3;\n\t"
+        "setp.eq.f32 pd, %1, %3;\n\t"
+        "selp.b32 %0, %5, %6, pu;\n\t"
+        "selp.b32 %0, %4, %0, pd;\n\t}"
+        : "=r"(r)
+        : "f"(d), "f"(u), "f"(m), "r"(sd), "r"(su), "r"(sl));
+    return r;
+}
+
 // lexicographic (cost, col): "a better than b"
 __device__ __forceinline__ bool better(float ca, int ja, float cb, int jb) {
     return ca < cb || (ca == cb && ja < jb);
@@ -421,7 +436,7 @@ __device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, W
             if constexpr (TRACE) {
                 const int su = R.S[0][ku];
                 const int sdg = (w == 0) ? psd[0] : R.S[0][kd];
-                const int sv = (dg == m) ? sdg : ((up == m) ? su : sl[0]);
+                const int sv = start_sel(dg, up, m, sdg, su, sl[0]);
                 R.S[0][kd] = sv;
                 sl[0] = sv;
             }
@@ -446,8 +461,8 @@ __device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, W
                     const int su0 = R.S[c0][ku], su1 = R.S[c1][ku];
                     const int sd0 = (w == 0) ? psd[c0] : R.S[c0][kd];
                     const int sd1 = (w == 0) ? psd[c1] : R.S[c1][kd];
-                    const int sv0 = (d0 == m0) ? sd0 : ((u0 == m0) ? su0 : sl[c0]);
-                    const int sv1 = (d1 == m1) ? sd1 : ((u1 == m1) ? su1 : sl[c1]);
+                    const int sv0 = start_sel(d0, u0, m0, sd0, su0, sl[c0]);
+                    const int sv1 = start_sel(d1, u1, m1, sd1, su1, sl[c1]);
                     R.S[c0][kd] = sv0;
                     R.S[c1][kd] = sv1;
                     sl[c0] = sv0;

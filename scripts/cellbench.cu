@@ -9,6 +9,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o cellbench cellbench.cu
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 constexpr int WC = 15, U = WC + 1, PERIODS = 4096;
 
@@ -16,13 +17,56 @@ __device__ __forceinline__ unsigned long long pk(float a, float b) {
     unsigned long long r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b)); return r; }
 __device__ __forceinline__ float lo32(unsigned long long r) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); (void)b; return a; }
 __device__ __forceinline__ float hi32(unsigned long long r) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); (void)a; return b; }
-__device__ __forceinline__ float half(unsigned long long r, int h) { return h ? hi32(r) : lo32(r); }
+__device__ __forceinline__ float halfsel(unsigned long long r, int h) { return h ? hi32(r) : lo32(r); }
 __device__ __forceinline__ unsigned long long swp(unsigned long long r) { return pk(hi32(r), lo32(r)); }
 __device__ __forceinline__ float min3f(float a, float b, float c) { return fminf(fminf(a, b), c); }
 __host__ __device__ constexpr int slot(int w, int h) { return ((w - h) % U + U) % U; }
 
 template <int I, int N_, class F> __device__ __forceinline__ void sfor(F&& f) {
     if constexpr (I < N_) { f(std::integral_constant<int, I>{}); sfor<I + 1, N_>(f); } }
+
+// MODE 5: fp16x2 cells (the paper's __half2 precision): two chains per
+// 32-bit register, HADD2 + 2 HMNMX2 + HFMA2 per 2 cells.  WCH columns per chain.
+constexpr int WCH = 31, UH = WCH + 1;
+__host__ __device__ constexpr int sloth(int w, int h) { return ((w - h) % UH + UH) % UH; }
+__global__ void __launch_bounds__(128) bench_half(float* out, float seed) {
+    const int lane = threadIdx.x & 31;
+    __half2 D[UH], Y[WCH];
+#pragma unroll
+    for (int k = 0; k < UH; ++k) D[k] = __floats2half2_rn(seed * k, seed * k + 1);
+#pragma unroll
+    for (int w = 0; w < WCH; ++w) Y[w] = __floats2half2_rn(seed * w * 0.5f, -seed * w);
+    __half2 right = __floats2half2_rn(seed, seed), pd = __floats2half2_rn(0.f, 0.f);
+    __half2 xx = __floats2half2_rn(seed + lane, seed - lane);
+    const __half2 step = __floats2half2_rn(0.25f, -0.25f);
+#pragma unroll 1
+    for (int it = 0; it < PERIODS; ++it) {
+        sfor<0, UH>([&](auto hc) {
+            constexpr int h = decltype(hc)::value;
+            const unsigned rs = __shfl_up_sync(0xffffffffu, *reinterpret_cast<unsigned*>(&right), 1);
+            __half2 l = __lows2half2(*reinterpret_cast<const __half2*>(&rs), right);   // (lane-1's chain 1, my chain 0)
+            const __half2 npd = l;
+#pragma unroll
+            for (int w = 0; w < WCH; ++w) {
+                const int ku = sloth(w, h), kd = sloth(w - 1, h);
+                const __half2 u = D[ku];
+                const __half2 d = w == 0 ? pd : D[kd];
+                const __half2 m = __hmin2(__hmin2(d, u), l);
+                const __half2 t = __hsub2(xx, Y[w]);
+                const __half2 v = __hfma2(t, t, m);
+                D[kd] = v;
+                l = v;
+            }
+            pd = npd;
+            right = l;
+            xx = __hadd2(xx, step);
+        });
+    }
+    float acc = __low2float(right) + __high2float(right);
+#pragma unroll
+    for (int k = 0; k < UH; ++k) acc += __low2float(D[k]) + __high2float(D[k]);
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(128) bench(float* out, float seed) {
@@ -74,14 +118,14 @@ __global__ void __launch_bounds__(128) bench(float* out, float seed) {
                     Ds0[kd] = v0; Ds1[kd] = v1; l0 = v0; l1 = v1;
                 } else {
                     const int o = (MODE == 1) ? (w & 1) : 0, op = (MODE == 1) ? ((w + 1) & 1) : 0;
-                    const float u0 = half(D[ku], o), u1 = half(D[ku], o ^ 1);
-                    const float d0 = w == 0 ? pd0 : half(D[kd], op), d1 = w == 0 ? pd1 : half(D[kd], op ^ 1);
+                    const float u0 = halfsel(D[ku], o), u1 = halfsel(D[ku], o ^ 1);
+                    const float d0 = w == 0 ? pd0 : halfsel(D[kd], op), d1 = w == 0 ? pd1 : halfsel(D[kd], op ^ 1);
                     const float m0 = min3f(d0, u0, l0), m1 = min3f(d1, u1, l1);
                     unsigned long long tt, vv;
                     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(o ? xs : xx), "l"(Y[w]));
                     asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(vv) : "l"(tt), "l"(o ? pk(m1, m0) : pk(m0, m1)));
                     D[kd] = vv;
-                    l0 = half(vv, o); l1 = half(vv, o ^ 1);
+                    l0 = halfsel(vv, o); l1 = halfsel(vv, o ^ 1);
                 }
             }
             pd0 = npd0; pd1 = npd1;
@@ -112,7 +156,27 @@ template <int MODE> void run(int warps_per_sm) {
     cudaFree(out);
 }
 
-int main() {
+void run_half(int warps_per_sm) {
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int blocks = sms * warps_per_sm / 4;
+    float* out; cudaMalloc(&out, sizeof(float) * blocks * 128);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    bench_half<<<blocks, 128>>>(out, 1e-3f);
+    cudaEventRecord(a);
+    bench_half<<<blocks, 128>>>(out, 1e-3f);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    const double cells = (double)blocks * 128 * PERIODS * UH * WCH * 2;
+    printf("%-12s warps/SM=%2d : %7.0f GCUPS  (%s)\n", "half2", warps_per_sm, cells / (ms * 1e-3) / 1e9,
+           cudaGetErrorString(cudaGetLastError()));
+    cudaFree(out);
+}
+
+int main(int argc, char** argv) {
+    if (argc > 1) {   // half2 only
+        for (int w : {8, 12, 16, 24, 32}) run_half(w);
+        return 0;
+    }
     for (int w : {12, 16, 24}) { run<0>(w); run<1>(w); run<2>(w); run<3>(w); run<4>(w); }
     for (int w : {12, 16, 24}) { run<0>(w); run<1>(w); run<2>(w); run<3>(w); run<4>(w); }
     return 0;

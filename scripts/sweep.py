@@ -7,6 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2403_06931_b200 as sd
 from datagen import nanopore_queries, nanopore_reference
 
+TRACE = bool(int(os.environ.get("TRACE", "0")))
 Z = int(os.environ.get("Z", 512)); N = int(os.environ.get("N", 2000)); M = int(os.environ.get("M", 1_000_000))
 dev = torch.device("cuda", 0)
 Y = torch.from_numpy(nanopore_reference(M, 3)).to(dev)
@@ -20,12 +21,12 @@ for cfg in configs:
     try:
         with sd.options(**cfg):
             for _ in range(2):
-                c, e = sd.batch(Q)
+                c, e = (sd.traceback(Q)[:2] if TRACE else sd.batch(Q))
             torch.cuda.synchronize()
             t = time.perf_counter()
             reps = 3
             for _ in range(reps):
-                c, e = sd.batch(Q)
+                c, e = (sd.traceback(Q)[:2] if TRACE else sd.batch(Q))
             torch.cuda.synchronize()
             dt = (time.perf_counter() - t) / reps
         same = None
