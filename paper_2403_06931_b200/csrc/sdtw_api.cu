@@ -161,11 +161,11 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     int WC = W / C;
     if (!pick_kernel(C, WC, true, false, false, dual))
         return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) + " for this chain layout" +
-                                    (C == 4 ? " (28)" : C == 2 ? " (14, 30, 62)" : " (7, 15)"));
+                                    (C == 4 ? " (28)" : C == 2 ? " (14, 30)" : " (7, 15)"));
     const int64_t units = dual ? (Z + 1) / 2 : Z;
     int GW = o.lanes > 0 ? o.lanes : 4;
     int CL = o.cluster > 0 ? o.cluster : 1;
-    if (GW < 1 || GW > (dual ? 12 : (WC >= 31 ? 4 : 8)) || CL < 1 || CL > 16 || (dual && CL != 1))
+    if (GW < 1 || GW > (dual ? 12 : 8) || CL < 1 || CL > 16 || (dual && CL != 1))
         return fail(SDTW_E_ARG, "lanes / cluster out of range for this kernel");
     // chunk = whole rotation periods (U = WC+1 steps), about the requested size
     const int U = WC + 1;

@@ -13,7 +13,6 @@ DpKernel pick_dp_c2(int WC, bool fma, bool cl) {
     switch (WC) {
         case 7: return pick_w<7>(fma, cl);
         case 15: return pick_w<15>(fma, cl);
-        case 31: return pick_w<31>(fma, cl);     // 32-step rotation, <= 4 warps per CTA (launch bounds)
         default: return nullptr;
     }
 }
