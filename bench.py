@@ -203,7 +203,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--path", action="store_true",
-                    help="step = sdtw_path (start index + full warp path, SURVEY NEXT-2); 1 GPU")
+                    help="step = sdtw_path (start index + full warp path, SURVEY NEXT-2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -234,13 +234,11 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    if args.path and world > 1:
-        raise SystemExit("--path runs on one GPU")
     trace = trace or args.path
 
     def step():
         if world > 1:
-            return distributed_batch(Qd, traceback=trace, pre_sharded=True, device=dev)
+            return distributed_batch(Qd, traceback=trace, pre_sharded=True, device=dev, path=args.path)
         if args.path:
             return sd.path(Qd)
         return sd.traceback(Qd) if trace else sd.batch(Qd)
@@ -313,7 +311,7 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             if world > 1:
-                distributed_batch(Qh.numpy(), traceback=trace, pre_sharded=True, device=dev)
+                distributed_batch(Qh.numpy(), traceback=trace, pre_sharded=True, device=dev, path=args.path)
             else:
                 api(Qh.numpy())
             e1.record(stream)
@@ -348,10 +346,11 @@ def main():
             "e2e": e2e, "cpu_baseline": cpu,
         }
         if args.path:
-            c, e, st, lo, hi = step()
+            import torch as _t
+            c, e, st, lo, hi = [_t.as_tensor(np.asarray(a.cpu() if hasattr(a, "cpu") else a)) for a in step()]
             L = (e - st + 1).double()
             line["path"] = {"window_cells_per_step": float((L * N).sum().item()),
-                            "path_cells_per_step": float((hi - lo + 1).double().sum().item()),
+                            "path_cells_per_step": float((hi.double() - lo.double() + 1).sum().item()),
                             "step_ms_incl_path": tot_ms / args.steps, "dp_kernel_ms": dp_avg,
                             "non_dp_share": 1.0 - dp_avg / (tot_ms / args.steps)}
             line["config"]["workload"] += " + full warp path (sdtw_path)"

@@ -7,7 +7,8 @@ the per-query records are exchanged with ONE all-gather (NCCL over
 NVLink/NVSwitch on GPUs, gloo in the CPU tests).  The reference is never split:
 a warp path may span any length of it.
 
-Record layout (int64 x 3 per query): [fp32 cost bits, end, start-or--1].
+Record layout (int64 x 3 per query): [fp32 cost bits, end, start-or--1]; with the full
+warp path (sdtw_path) a second all-gather moves the per-row column ranges (int32 x 2 x N).
 """
 from __future__ import annotations
 
@@ -48,14 +49,28 @@ def _unpack(rec: torch.Tensor, Z: int, want_start: bool):
     return cost, end, start
 
 
+def _gather(t: torch.Tensor, world: int, group):
+    full = torch.empty((t.shape[0] * world, *t.shape[1:]), dtype=t.dtype, device=t.device)
+    try:
+        dist.all_gather_into_tensor(full, t, group=group)
+    except (RuntimeError, NotImplementedError, AttributeError):
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t, group=group)
+        full = torch.cat(parts, 0)
+    return full
+
+
 def distributed_batch(Q, group=None, traceback: bool = False,
-                      fn: Optional[Callable] = None, device=None, pre_sharded: bool = False):
+                      fn: Optional[Callable] = None, device=None, pre_sharded: bool = False,
+                      path: bool = False):
     """Shard Q [Z, N] over the ranks of `group`, compute locally, all-gather results.
 
-    fn(Q_shard) -> (cost, end[, start]); default: this package's CUDA ``batch`` /
-    ``traceback``.  With pre_sharded=True, Q is already this rank's shard and every
-    rank holds the same number of queries (global Z = world * Q.shape[0]).
-    Returns numpy (cost[Z], end[Z], start[Z] | None) on every rank."""
+    fn(Q_shard) -> (cost, end[, start[, path_lo, path_hi]]); default: this package's CUDA
+    ``batch`` / ``traceback`` / ``path``.  With pre_sharded=True, Q is already this rank's
+    shard and every rank holds the same number of queries (global Z = world *
+    Q.shape[0]).  Returns numpy (cost[Z], end[Z], start[Z] | None) on every rank, plus
+    (path_lo[Z, N], path_hi[Z, N]) int32 when path=True (a second all-gather)."""
+    traceback = traceback or path
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     if pre_sharded:
@@ -67,22 +82,26 @@ def distributed_batch(Q, group=None, traceback: bool = False,
         lo, hi, per = shard_bounds(Z, world, rank)
     if fn is None:
         import paper_2403_06931_b200 as sd
-        fn = sd.traceback if traceback else sd.batch
+        fn = sd.path if path else (sd.traceback if traceback else sd.batch)
     if device is None:
         device = Q.device if isinstance(Q, torch.Tensor) else torch.device("cpu")
     if dist.get_backend(group) == "nccl" and device.type != "cuda":
         device = torch.device("cuda", torch.cuda.current_device())
+    N = int(Q.shape[1]) if len(Q.shape) > 1 else 1
     if hi > lo:
         out = fn(Q[lo:hi])
     else:
-        out = (np.empty(0, np.float32), np.empty(0, np.int64), np.empty(0, np.int64))
+        out = (np.empty(0, np.float32), np.empty(0, np.int64), np.empty(0, np.int64),
+               np.empty((0, N), np.int32), np.empty((0, N), np.int32))
     start = out[2] if traceback else None
     rec = _pack(out[0], out[1], start, per, device)
-    full = torch.empty((per * world, 3), dtype=torch.int64, device=device)
-    try:
-        dist.all_gather_into_tensor(full, rec, group=group)
-    except (RuntimeError, NotImplementedError, AttributeError):
-        parts = [torch.empty_like(rec) for _ in range(world)]
-        dist.all_gather(parts, rec, group=group)
-        full = torch.cat(parts, 0)
-    return _unpack(full, Z, traceback)
+    res = _unpack(_gather(rec, world, group), Z, traceback)
+    if not path:
+        return res
+    pth = torch.full((per, N, 2), -1, dtype=torch.int32)
+    n = hi - lo
+    if n:
+        for k, a in ((0, out[3]), (1, out[4])):
+            pth[:n, :, k] = torch.as_tensor(np.asarray(a.cpu() if isinstance(a, torch.Tensor) else a, np.int32))
+    full = _gather(pth.to(device), world, group)[:Z].cpu().numpy()
+    return res + (full[:, :, 0].copy(), full[:, :, 1].copy())

@@ -42,6 +42,52 @@ def _worker(rank, world, port, Z, traceback, out_q):
         dist.destroy_process_group()
 
 
+def _path_worker(rank, world, port, Z, out_q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2403_06931_b200.distributed import distributed_batch
+        rng = np.random.default_rng(9)
+        Y = rng.standard_normal(300).astype(np.float32)
+        Q = rng.standard_normal((Z, 12)).astype(np.float32)
+
+        def fn(Qs):
+            rs = [oracle.sdtw_path(q, Y) for q in np.asarray(Qs)]
+            return (np.array([r[0] for r in rs], np.float32), np.array([r[1] for r in rs], np.int64),
+                    np.array([r[2] for r in rs], np.int64), np.array([r[3] for r in rs], np.int32),
+                    np.array([r[4] for r in rs], np.int32))
+
+        out_q.put((rank,) + distributed_batch(Q, path=True, fn=fn))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("Z", [5, 1])
+def test_gloo_world2_path_matches_single_process(Z):
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_path_worker, args=(r, 2, port, Z, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(9)
+    Y = rng.standard_normal(300).astype(np.float32)
+    Q = rng.standard_normal((Z, 12)).astype(np.float32)
+    for _, cost, end, start, lo, hi in res:
+        for k in range(Z):
+            rc, re, rs, rlo, rhi = oracle.sdtw_path(Q[k], Y)
+            assert cost[k] == rc and end[k] == re and start[k] == rs
+            assert np.array_equal(lo[k], rlo) and np.array_equal(hi[k], rhi)
+
+
 @pytest.mark.parametrize("Z,traceback", [(7, False), (8, True), (1, True)])
 def test_gloo_world2_matches_single_process(Z, traceback):
     import oracle
