@@ -165,7 +165,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     const int64_t units = dual ? (Z + 1) / 2 : Z;
     int GW = o.lanes > 0 ? o.lanes : 4;
     int CL = o.cluster > 0 ? o.cluster : 1;
-    if (GW < 1 || GW > (dual ? 12 : 8) || CL < 1 || CL > 16 || (dual && CL != 1))
+    if (GW < 1 || GW > (dual ? 12 : (C == 4 ? 4 : 8)) || CL < 1 || CL > 16 || (dual && CL != 1))
         return fail(SDTW_E_ARG, "lanes / cluster out of range for this kernel");
     // chunk = whole rotation periods (U = WC+1 steps), about the requested size
     const int U = WC + 1;

@@ -41,6 +41,9 @@
 #include <type_traits>
 
 // Build-time knobs (A/B variants via -D; the defaults are the measured best)
+#ifndef SDTW_C4_MINB
+#define SDTW_C4_MINB 3           // resident 4-warp CTAs per SM the 4-chain kernels are sized for
+#endif
 #ifndef SDTW_SPIN_NS
 #define SDTW_SPIN_NS 256         // nanosleep per flow-control poll (r01 A/B: 256 > 64 by 0.8 %)
 #endif
@@ -569,7 +572,7 @@ __device__ __forceinline__ bool hits_row(int blo, int len, int row, int Pd) { re
 
 // ============================================================================ kernel
 template <int C, int WC, bool FMA, bool TRACE, bool CLUSTER>
-__global__ void __launch_bounds__(256, 2) sdtw_dp_kernel(const DpParams P) {
+__global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2) sdtw_dp_kernel(const DpParams P) {
     static_assert(C == 1 || C == 2 || C == 4, "chains per lane");
     static_assert(((WC + 1) & WC) == 0 && (32 * C) % (WC + 1) == 0 && (WC + 1) % C == 0,
                   "rotation period U = WC+1 must be a power of two dividing 32*C and divisible by C");
