@@ -294,6 +294,12 @@ def main():
             "dp_kernel_ms": dp_avg}
     if clocks.get("sm_mhz"):
         roof["frac_at_sampled_clock"] = achieved / (peak * clocks["sm_mhz"] / fmax)
+    if trace:
+        # the start-index cell needs 5 ALU-pipe ops (FMNMX3 + 2 FSETP + 2 SEL; the ALU pipe
+        # issues 16 lanes/clk/SMSP): that pipe, not issue, binds it (ncu: alu 72 % busy)
+        alu_peak = sms * 64 * fmax * 1e6 / 5.0 / 1e9
+        roof["alu_pipe_peak"] = alu_peak
+        roof["alu_pipe_frac"] = achieved / alu_peak
 
     # e2e: the same metric through the public API with host buffers (pinned), copies inside
     e2e = None

@@ -233,6 +233,7 @@ __device__ __forceinline__ unsigned long long cell2(unsigned long long xx, unsig
 // (reading G6): branch-free FSETP + SEL pairs (the ternary form compiled to a
 // BSSY/BRA/BSYNC diamond per cell -- 4.3x the instructions of the plain DP).
 __device__ __forceinline__ int start_sel(float d, float u, float m, int sd, int su, int sl) {
+    // (predicated moves instead of selp compile to the same FSETP + SEL)
     int r;
     asm("{\n\t.reg .pred pu, pd;\n\t"
         "setp.eq.f32 pu, %2, %3;\n\t"
