@@ -86,6 +86,18 @@ sdtw_status sdtw_batch(const float* Q, int64_t n_queries, int64_t N,
 sdtw_status sdtw_traceback(const float* Q, int64_t n_queries, int64_t N,
                            float* out_cost, int64_t* out_end, int64_t* out_start);
 
+/* Ragged batch (read-until style batches of variable-length
+ * reads).  Q holds the queries back to back, query q = Q[offsets[q] .. offsets[q+1]);
+ * offsets: n_queries+1 int64, offsets[0] == 0, strictly increasing (every query has >= 1
+ * sample); Q, offsets and the outputs may each be host or device pointers.  Per query the
+ * result is exactly what sdtw_batch / sdtw_traceback return for that query alone:
+ * out_cost, out_end, and out_start when out_start != NULL (start propagation on).  Each
+ * query is z-normalised with its own statistics.  The DP runs all lengths in one launch
+ * (per-query round period; persistent units scheduled by expected duration).
+ * Errors: SDTW_E_ARG (bad offsets, OPT_PACKED 3/4), plus those of sdtw_batch. */
+sdtw_status sdtw_batch_ragged(const float* Q, const int64_t* offsets, int64_t n_queries,
+                              float* out_cost, int64_t* out_end, int64_t* out_start);
+
 /* As sdtw_traceback, plus the full optimal warp path of every query (SURVEY.md
  * §8(f) NEXT-2; the walk-back of P:L35 from (N-1, out_end) with the tie rule
  * diag > up > left).  A monotone warp path visits a contiguous run of reference

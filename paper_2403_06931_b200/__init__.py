@@ -7,7 +7,7 @@ fallback: importing this package fails loudly when the library is missing, and
 every call raises when the CUDA path fails.
 
 Functions mirror the ABI names (minus the ``sdtw_`` prefix):
-``set_reference``, ``batch``, ``traceback``, ``path``, ``znormalize``, ``set_option``,
+``set_reference``, ``batch``, ``batch_ragged``, ``traceback``, ``path``, ``znormalize``, ``set_option``,
 ``get_option``, ``profile``, ``launch_count``, ``release``.
 Inputs may be torch tensors (CUDA or CPU) or numpy arrays.  torch supplies
 device memory and the current stream (passed as SDTW_OPT_STREAM).
@@ -34,6 +34,8 @@ _i64 = ctypes.c_int64
 _lib.sdtw_set_reference.argtypes = [ctypes.c_void_p, _i64]
 _lib.sdtw_batch.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p]
 _lib.sdtw_traceback.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+_lib.sdtw_batch_ragged.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _i64, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p]
 _lib.sdtw_path.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_void_p]
 _lib.sdtw_znormalize.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p]
@@ -43,7 +45,7 @@ _lib.sdtw_profile.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i
 _lib.sdtw_launch_count.restype = _i64
 _lib.sdtw_last_error.restype = ctypes.c_char_p
 _lib.sdtw_version.restype = ctypes.c_int
-for _n in ("sdtw_set_reference", "sdtw_batch", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
+for _n in ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
            "sdtw_set_option", "sdtw_get_option", "sdtw_profile"):
     getattr(_lib, _n).restype = ctypes.c_int
 
@@ -54,7 +56,7 @@ OPT_NORMALIZE, OPT_FMA, OPT_SEGMENT_W, OPT_LANES, OPT_CLUSTER, OPT_STREAM, OPT_P
 _STATUS = {0: "SDTW_OK", 1: "SDTW_E_ARG", 2: "SDTW_E_NOREF", 3: "SDTW_E_CUDA", 4: "SDTW_E_NOMEM",
            5: "SDTW_E_NONFINITE"}
 
-EXPORTED_SYMBOLS = ("sdtw_set_reference", "sdtw_batch", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
+EXPORTED_SYMBOLS = ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
                     "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_launch_count",
                     "sdtw_last_error", "sdtw_release", "sdtw_version")
 
@@ -162,6 +164,28 @@ def traceback(Q):
     _check(_lib.sdtw_traceback(ctypes.c_void_p(ptr), Z, N, ctypes.c_void_p(pc), ctypes.c_void_p(pe),
                                ctypes.c_void_p(ps)))
     return cost, end, start
+
+
+def batch_ragged(Q, offsets, start: bool = False):
+    """sdtw_batch_ragged: Q = queries back to back (1-D), query q = Q[offsets[q]:offsets[q+1]]
+    -> (cost, end) or (cost, end, start), each exactly the single-query result."""
+    keep, ptr, shape = _as_f32(Q)
+    torch = _torch()
+    if torch is not None and isinstance(offsets, torch.Tensor):
+        okeep = offsets.to(torch.int64).contiguous()
+        optr = okeep.data_ptr()
+        Z = okeep.numel() - 1
+    else:
+        okeep = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+        optr = okeep.ctypes.data
+        Z = okeep.shape[0] - 1
+    if Z < 0:
+        raise ValueError("offsets needs n_queries + 1 entries")
+    cost, end, st, (pc, pe, ps) = _outputs(keep, Z, start)
+    _bind_stream(keep)
+    _check(_lib.sdtw_batch_ragged(ctypes.c_void_p(ptr), ctypes.c_void_p(optr), Z, ctypes.c_void_p(pc),
+                                  ctypes.c_void_p(pe), ctypes.c_void_p(ps if start else 0)))
+    return (cost, end, st) if start else (cost, end)
 
 
 def path(Q):

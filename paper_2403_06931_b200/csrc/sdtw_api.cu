@@ -18,6 +18,7 @@
 #include <string>
 #include <algorithm>
 #include <vector>
+#include <queue>
 
 namespace {
 
@@ -54,6 +55,7 @@ struct Ctx {
     double* ws_part = nullptr;                      // reference partial sums + stats
     unsigned char* ws_sched = nullptr; size_t ws_sched_n = 0;   // persistent scheduling state
     unsigned char* ws_path = nullptr; size_t ws_path_n = 0;     // sdtw_path codes / row buffers / outputs
+    unsigned char* ws_rag = nullptr; size_t ws_rag_n = 0;       // ragged-batch offsets + lengths
     int* order_d = nullptr; size_t order_n = 0;     // unit grab order (device) and its key
     int64_t order_key[3] = {-1, -1, -1};
     int* flag_d = nullptr;
@@ -144,11 +146,18 @@ struct LaunchCfg {
     int persistent, S, workers;
     int dual;        // two queries per lane (chains per lane = C)
     int64_t units;   // rings per batch: queries, or query pairs when dual
+    int need;        // V + (G+1)K: smallest ring-safe round period (ragged batches: per query)
+};
+
+// Ragged batch descriptor (host): offsets[Z+1], the longest and shortest query.
+struct Ragged {
+    const std::vector<int64_t>* off = nullptr;
+    int64_t nmin = 0;
 };
 
 // Schedule choice.  OPT_PACKED: 0 scalar (C=1), 1 two packed chains (C=2), 2 four
 // chains (C=4), 3 dual-query x 2 chains, 4 dual-query x 1 chain; -1 auto.
-sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cfg) {
+sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cfg, const Ragged* rg = nullptr) {
     const Options& o = g_opt;
     // auto: two packed chains (f32x2) for cost/end; scalar strips for the start-index
     // variant, whose per-cell start selects double the registers per slot (r01 sweep at
@@ -173,7 +182,8 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     const int64_t V = 32LL * C * G;
     // chunk: 64 steps when the query is long enough that the round period stays N
     // (Pd >= V + (G+1)K), else 32 (r01 sweep: K=64 +1.5% over 32, K=128 -12%)
-    const int Kreq = o.chunk > 0 ? o.chunk : (N >= V + (int64_t)(G + 1) * 64 ? 64 : 32);
+    const int64_t Nk = rg ? rg->nmin : N;                // ragged: the shortest query decides
+    const int Kreq = o.chunk > 0 ? o.chunk : (Nk >= V + (int64_t)(G + 1) * 64 ? 64 : 32);
     const int KU = (dual ? 1 : SDTW_FAST_PERIODS) * U;   // chunk = whole fast/slow decision windows
     const int K = KU * std::max(1, (Kreq + KU / 2) / KU);
     const int64_t need = V + (int64_t)(G + 1) * K;
@@ -189,7 +199,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     const sdtw::SmemLayout L = dual ? sdtw::smem_layout_q(C, WC, trace, GW, (int)Pd, RS)
                                     : sdtw::smem_layout(C, WC, trace, GW, (int)Pd, RS);
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
-    *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0, dual ? 1 : 0, units};
+    *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0, dual ? 1 : 0, units, (int)need};
     // Persistent scheduling (default when a cluster is not requested): k resident CTAs
     // per SM, k = min(occupancy, rings / SMs), pull (ring, round-segment) units, so every
     // SM carries the same load whatever the batch size mod #SMs is.
@@ -279,8 +289,47 @@ struct BatchDev {
     const int64_t* start = nullptr;
 };
 
+// Ragged batches: units of one ring take time ~ its round period, so the wave model
+// above no longer holds.  Event simulation of W workers with per-ring unit durations
+// w[q]: a free worker takes the ready chain (predecessor segment finished) with the most
+// remaining work, else waits for the earliest chain to become ready.
+std::vector<int> unit_order_weighted(int64_t R, int S, int64_t W, const std::vector<double>& w) {
+    std::vector<int> order;
+    order.reserve((size_t)(R * S));
+    std::vector<int> next(R, 0);
+    typedef std::pair<double, int64_t> Item;
+    std::priority_queue<Item> ready;                                              // (remaining work, q)
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> pending;       // (ready time, q)
+    std::priority_queue<double, std::vector<double>, std::greater<double>> workers;  // free times
+    for (int64_t q = 0; q < R; ++q) ready.push(Item(w[q] * S, q));
+    for (int64_t k = 0; k < W; ++k) workers.push(0.0);
+    for (int64_t left = R * S; left > 0; --left) {
+        double t = workers.top();
+        workers.pop();
+        while (!pending.empty() && pending.top().first <= t) {
+            const int64_t q = pending.top().second;
+            pending.pop();
+            ready.push(Item(w[q] * (S - next[q]), q));
+        }
+        if (ready.empty()) {                       // idle until the earliest chain is ready
+            t = pending.top().first;
+            const int64_t q = pending.top().second;
+            pending.pop();
+            ready.push(Item(w[q] * (S - next[q]), q));
+        }
+        const int64_t q = ready.top().second;
+        ready.pop();
+        order.push_back((int)((int64_t)next[q] * R + q));
+        const double fin = t + w[q];
+        ++next[q];
+        if (next[q] < S) pending.push(Item(fin, q));
+        workers.push(fin);
+    }
+    return order;
+}
+
 sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
-                      int64_t* out_start, bool trace, BatchDev* dev_out = nullptr) {
+                      int64_t* out_start, bool trace, BatchDev* dev_out = nullptr, Ragged rg = Ragged()) {
     if (N < 1 || Z < 0) return fail(SDTW_E_ARG, "N must be >= 1 and n_queries >= 0");
     if (Z > 0 && (!Q || !out_cost || !out_end || (trace && !out_start)))
         return fail(SDTW_E_ARG, "NULL pointer");
@@ -297,13 +346,34 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     const int64_t launches0 = g_launches.load();
 
     LaunchCfg cfg;
-    s = plan(*ctx, Z, N, trace, &cfg);
+    s = plan(*ctx, Z, N, trace, &cfg, rg.off ? &rg : nullptr);
     if (s != SDTW_OK) return s;
+    if (rg.off && cfg.dual) return fail(SDTW_E_ARG, "ragged batches need OPT_PACKED in {0, 1, 2}");
 
     const int kq = ptr_kind(Q), kc = ptr_kind(out_cost), ke = ptr_kind(out_end);
     const int ks = trace ? ptr_kind(out_start) : 1;
     if (kq < 0 || kc < 0 || ke < 0 || ks < 0) return fail(SDTW_E_ARG, "device pointer on another device");
-    const size_t nel = (size_t)Z * (size_t)N;
+    const size_t nel = rg.off ? (size_t)(*rg.off)[Z] : (size_t)Z * (size_t)N;
+    // ragged: offsets and lengths on the device (one small H2D)
+    const int64_t* qoff_d = nullptr;
+    const int* qlen_d = nullptr;
+    if (rg.off) {
+        const size_t bytes = (size_t)(Z + 1) * 8 + (size_t)Z * 4;
+        if (bytes > ctx->ws_rag_n) {
+            if (ctx->ws_rag) cudaFree(ctx->ws_rag);
+            ctx->ws_rag = nullptr;
+            ctx->ws_rag_n = 0;
+            CK(cudaMalloc(&ctx->ws_rag, bytes));
+            ctx->ws_rag_n = bytes;
+        }
+        std::vector<unsigned char> hb(bytes);
+        memcpy(hb.data(), rg.off->data(), (size_t)(Z + 1) * 8);
+        int* hl = reinterpret_cast<int*>(hb.data() + (size_t)(Z + 1) * 8);
+        for (int64_t q = 0; q < Z; ++q) hl[q] = (int)((*rg.off)[q + 1] - (*rg.off)[q]);
+        CK(cudaMemcpy(ctx->ws_rag, hb.data(), bytes, cudaMemcpyHostToDevice));
+        qoff_d = reinterpret_cast<const int64_t*>(ctx->ws_rag);
+        qlen_d = reinterpret_cast<const int*>(ctx->ws_rag + (size_t)(Z + 1) * 8);
+    }
 
     const float* qd = Q;
     if (kq == 0) {
@@ -319,10 +389,10 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         s = grow(&ctx->ws_x, &ctx->ws_x_n, nel + (pad ? (size_t)N : 0));
         if (s != SDTW_OK) return s;
         if (pad) CK(cudaMemsetAsync(ctx->ws_x + nel, 0, (size_t)N * sizeof(float), st));
-        sdtw::znorm_rows_kernel<<<(unsigned)Z, 256, 0, st>>>(qd, ctx->ws_x, N, o.normalize, ctx->flag_d);
+        sdtw::znorm_rows_kernel<<<(unsigned)Z, 256, 0, st>>>(qd, ctx->ws_x, N, o.normalize, ctx->flag_d, qoff_d);
         xd = ctx->ws_x;
     } else {
-        sdtw::znorm_rows_kernel<<<(unsigned)Z, 256, 0, st>>>(qd, const_cast<float*>(qd), N, 0, ctx->flag_d);
+        sdtw::znorm_rows_kernel<<<(unsigned)Z, 256, 0, st>>>(qd, const_cast<float*>(qd), N, 0, ctx->flag_d, qoff_d);
     }
     CK(cudaGetLastError());
     g_launches++;
@@ -359,6 +429,9 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.S = cfg.S;
     p.counter = nullptr;
     p.order = nullptr;
+    p.qoff = qoff_d;
+    p.qlen = qlen_d;
+    p.need = cfg.need;
     p.seg_done = nullptr;
     p.bnd_g = nullptr;
     p.cand = nullptr;
@@ -375,8 +448,17 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         p.cand = b + 256 + done_b;
         p.bnd_g = static_cast<unsigned char*>(p.cand) + 16 * (size_t)Z * cfg.S;
         CK(cudaMemsetAsync(b, 0, 256 + done_b, st));
-        if (ctx->order_key[0] != (int64_t)R || ctx->order_key[1] != cfg.S || ctx->order_key[2] != cfg.workers) {
-            const std::vector<int> ord = unit_order((int64_t)R, cfg.S, cfg.workers);
+        if (rg.off || ctx->order_key[0] != (int64_t)R || ctx->order_key[1] != cfg.S ||
+            ctx->order_key[2] != cfg.workers) {
+            std::vector<int> ord;
+            if (rg.off) {
+                std::vector<double> w(R);
+                for (int64_t q = 0; q < (int64_t)R; ++q)
+                    w[q] = (double)std::max<int64_t>((*rg.off)[q + 1] - (*rg.off)[q], cfg.need);
+                ord = unit_order_weighted((int64_t)R, cfg.S, cfg.workers, w);
+            } else {
+                ord = unit_order((int64_t)R, cfg.S, cfg.workers);
+            }
             if (ord.size() > ctx->order_n) {
                 if (ctx->order_d) cudaFree(ctx->order_d);
                 ctx->order_d = nullptr;
@@ -385,7 +467,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
                 ctx->order_n = ord.size();
             }
             CK(cudaMemcpy(ctx->order_d, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice));
-            ctx->order_key[0] = (int64_t)R;
+            ctx->order_key[0] = rg.off ? -1 : (int64_t)R;             // ragged orders are not cached
             ctx->order_key[1] = cfg.S;
             ctx->order_key[2] = cfg.workers;
         }
@@ -562,6 +644,37 @@ sdtw_status sdtw_traceback(const float* Q, int64_t n_queries, int64_t N, float* 
     return run_batch(Q, n_queries, N, out_cost, out_end, out_start, true);
 }
 
+sdtw_status sdtw_batch_ragged(const float* Q, const int64_t* offsets, int64_t n_queries, float* out_cost,
+                              int64_t* out_end, int64_t* out_start) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (n_queries < 0) return fail(SDTW_E_ARG, "n_queries must be >= 0");
+    if (n_queries == 0) return run_batch(Q, 0, 1, out_cost, out_end, out_start, out_start != nullptr);
+    if (!offsets) return fail(SDTW_E_ARG, "NULL pointer");
+    if (n_queries > 0x7fffffff) return fail(SDTW_E_ARG, "sizes exceed int32");
+    const int ko = ptr_kind(offsets);
+    if (ko < 0) return fail(SDTW_E_ARG, "device pointer on another device");
+    std::vector<int64_t> off((size_t)n_queries + 1);
+    if (ko) {
+        const cudaError_t e = cudaMemcpy(off.data(), offsets, off.size() * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(offsets)");
+    } else {
+        memcpy(off.data(), offsets, off.size() * 8);
+    }
+    if (off[0] != 0) return fail(SDTW_E_ARG, "offsets[0] must be 0");
+    int64_t nmax = 0, nmin = INT64_MAX;
+    for (int64_t q = 0; q < n_queries; ++q) {
+        const int64_t n = off[q + 1] - off[q];
+        if (n < 1) return fail(SDTW_E_ARG, "every query needs >= 1 sample (offsets strictly increasing)");
+        nmax = std::max(nmax, n);
+        nmin = std::min(nmin, n);
+    }
+    if (nmax > 0x7fffffff) return fail(SDTW_E_ARG, "query length exceeds int32");
+    Ragged rg;
+    rg.off = &off;
+    rg.nmin = nmin;
+    return run_batch(Q, n_queries, nmax, out_cost, out_end, out_start, out_start != nullptr, nullptr, rg);
+}
+
 sdtw_status sdtw_path(const float* Q, int64_t n_queries, int64_t N, float* out_cost, int64_t* out_end,
                       int64_t* out_start, int32_t* path_lo, int32_t* path_hi) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -683,6 +796,7 @@ void sdtw_release(void) {
     cudaFree(c.ws_part);
     cudaFree(c.ws_sched);
     cudaFree(c.ws_path);
+    cudaFree(c.ws_rag);
     cudaFree(c.order_d);
     cudaFree(c.flag_d);
     cudaFreeHost(c.flag_h);

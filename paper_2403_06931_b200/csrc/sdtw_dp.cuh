@@ -71,6 +71,11 @@ struct DpParams {
     int persistent;
     int S;
     int Zq;                // real number of queries (dual-query kernel: P.Z counts pairs)
+    // ragged batches: query q is X[qoff[q] .. qoff[q]+qlen[q]) with round
+    // period max(qlen[q], need); N / Pd above are then the maxima (shared-memory sizing)
+    const int64_t* qoff;   // nullptr = fixed length N, query q at X + q*N
+    const int* qlen;
+    int need;              // V + (G+1)K: the smallest ring-safe round period
     int* counter;
     const int* order;      // grab order of the units (nullptr = identity), see unit_order() in sdtw_api.cu
     int* seg_done;
@@ -592,8 +597,8 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     const int G = GW * CL;
     const int gw = rank * GW + warp;
     const int V = 32 * C * G;
-    const int Pd = P.Pd, N = P.N, K = P.K, RS = P.RS;
-    const SmemLayout L = smem_layout(C, WC, TRACE, GW, Pd, RS);
+    const int PdMax = P.Pd, K = P.K, RS = P.RS;
+    const SmemLayout L = smem_layout(C, WC, TRACE, GW, PdMax, RS);
 
     int* pp = reinterpret_cast<int*>(smem + L.off_ctr);        // producer progress seen by warp w
     int* cp = pp + 32;                                          // consumer progress of w's successor
@@ -664,13 +669,20 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         if (unit_iter > 0) break;
         q = blockIdx.x / CL;
     }
+    // query length and round period of this unit (ragged batches: per query)
+    int N = P.N, Pd = PdMax;
+    const float* xq = P.X + (long)q * N;
+    if (P.qlen) {
+        N = P.qlen[q];
+        Pd = max(N, P.need);
+        xq = P.X + P.qoff[q];
+    }
     const int Pl = pb - pa;                                 // rounds in this unit
     const int Mtot_bands = Pl * Pd;
 
     // ---- prologue: query rows -> smem, boundary ring (+inf, or the previous
     // segment's last column), counters
-    const float* xq = P.X + (long)q * N;
-    const E* bg = reinterpret_cast<const E*>(P.bnd_g) + (long)q * Pd;
+    const E* bg = reinterpret_cast<const E*>(P.bnd_g) + (long)q * PdMax;
     for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
         float* dst = xs + (long)xrow_index(r, Pd, NC) * XC;
 #pragma unroll
@@ -961,7 +973,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     if (P.persistent) {
         // hand this segment's last column to the next segment of the query
         if (seg + 1 < P.S) {
-            E* bo = reinterpret_cast<E*>(P.bnd_g) + (long)q * Pd;
+            E* bo = reinterpret_cast<E*>(P.bnd_g) + (long)q * PdMax;
             for (int r = threadIdx.x; r < Pd; r += blockDim.x) bo[r] = bnd[r];
         }
         __syncthreads();

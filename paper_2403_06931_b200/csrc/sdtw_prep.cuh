@@ -51,11 +51,18 @@ __device__ __forceinline__ bool stats_to_affine(double sum, double sumsq, double
 }
 
 // One CTA per series.  Normalises (normalize != 0) or only checks finiteness.
+// offsets != nullptr: ragged batch, series b = in[offsets[b] .. offsets[b+1]).
 __global__ void __launch_bounds__(256) znorm_rows_kernel(const float* __restrict__ in, float* out,
-                                                         int64_t len, int normalize, int* flag) {
+                                                         int64_t len, int normalize, int* flag,
+                                                         const int64_t* offsets = nullptr) {
     __shared__ double scratch[64];
-    const float* x = in + (int64_t)blockIdx.x * len;
-    float* z = out + (int64_t)blockIdx.x * len;
+    int64_t base = (int64_t)blockIdx.x * len;
+    if (offsets) {
+        base = offsets[blockIdx.x];
+        len = offsets[blockIdx.x + 1] - base;
+    }
+    const float* x = in + base;
+    float* z = out + base;
     double s = 0.0, s2 = 0.0;
     bool bad = false;
     for (int64_t k = threadIdx.x; k < len; k += blockDim.x) {
