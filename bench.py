@@ -133,6 +133,11 @@ def _workload(cfg_name: str, rank: int, world: int, scaling: str):
         Zl = max(0, min(Z, first + per) - first)
         Zg = Z
     Y = nanopore_reference(M, seed)
+    if cfg.get("ragged"):
+        from datagen import nanopore_ragged
+        Q, off = nanopore_ragged(Zl, M, seed, *cfg["ragged"], first_query=first)
+        return Q, Y, dict(Z=Zg, Z_local=Zl, N=N, M=M, seed=seed, start=cfg["start"], offsets=off,
+                          cells_local=float(off[-1]) * M)
     Q = nanopore_queries(Zl, N, M, seed, first_query=first)
     return Q, Y, dict(Z=Zg, Z_local=Zl, N=N, M=M, seed=seed, start=cfg["start"])
 
@@ -180,6 +185,8 @@ def cpu_baseline_leg(args, Q, Y, N):
     import oracle
     threads = os.cpu_count() or 1
     Ms = int(min(Y.shape[0], max(2000, 2.0e9 / N)))
+    if Q.ndim == 1:   # ragged batch: time the oracle on a slab of the same samples cut at length N
+        Q = Q[:(Q.shape[0] // N) * N].reshape(-1, N)
     nq = min(Q.shape[0], threads)
     Yn = oracle.znorm(Y[:Ms][None])[0]
     Qn = oracle.znorm(Q[:nq])
@@ -236,7 +243,15 @@ def main():
 
     trace = trace or args.path
 
+    ragged = "offsets" in w
+    if ragged:
+        if world > 1 or args.path:
+            raise SystemExit("ragged configs run on one GPU without --path")
+        off_d = torch.from_numpy(w["offsets"]).to(dev)
+
     def step():
+        if ragged:
+            return sd.batch_ragged(Qd, off_d)
         if world > 1:
             return distributed_batch(Qd, traceback=trace, pre_sharded=True, device=dev, path=args.path)
         if args.path:
@@ -271,7 +286,7 @@ def main():
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
-    cells_step = float(w["Z"]) * N * M
+    cells_step = w["cells_local"] * world if ragged else float(w["Z"]) * N * M
     value = cells_step * args.steps / (tot_ms / 1e3) / 1e9
 
     # roofline of the dominant kernel (the DP kernel), measured on its own stream
@@ -285,7 +300,7 @@ def main():
     peak = sms * LANES_PER_SM * fmax * 1e6 / k / 1e9
     peak3 = sms * LANES_PER_SM * fmax * 1e6 / 3.0 / 1e9
     dp_avg = statistics.mean(dp_ms)
-    achieved = float(w["Z_local"]) * N * M / (dp_avg / 1e3) / 1e9
+    achieved = (w["cells_local"] if ragged else float(w["Z_local"]) * N * M) / (dp_avg / 1e3) / 1e9
     clocks = sampler.summary()
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "GCUPS", "frac": achieved / peak,
             "traffic": _traffic(args.config, w), "sass_per_cell": k, "peak_source": "%s sm_max_mhz=%.0f x %d SMs x %d lanes / %g"
@@ -306,6 +321,8 @@ def main():
     if not args.no_e2e:
         Qh = torch.from_numpy(Q).pin_memory()
         api = sd.path if args.path else (sd.traceback if trace else sd.batch)
+        if ragged:
+            api = lambda q: sd.batch_ragged(q, w["offsets"])  # noqa: E731
         api(Qh.numpy())
         ts = []
         for i in range(max(1, min(args.steps, 3))):

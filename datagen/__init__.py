@@ -27,6 +27,7 @@ __all__ = [
     "nanopore_reference",
     "nanopore_queries",
     "nanopore_workload",
+    "nanopore_ragged",
     "cbf_series",
     "cbf_reference",
     "cbf_batch",
@@ -43,6 +44,8 @@ CONFIGS = {
     "c5_1000": dict(Z=512, N=1000, M=1_000_000, seed=5, start=True),
     "c5_4000": dict(Z=512, N=4000, M=1_000_000, seed=5, start=True),
     "c5_8000": dict(Z=512, N=8000, M=1_000_000, seed=5, start=True),
+    # NEXT-4: a ragged batch of reads, lengths log-uniform in [500, 8000] (N = mean, info only)
+    "c6_ragged": dict(Z=512, N=2700, M=1_000_000, seed=6, start=False, ragged=(500, 8000)),
 }
 
 _K = 6  # k-mer order of the level table
@@ -107,6 +110,20 @@ def nanopore_queries(Z: int, N: int, M: int, seed: int,
         offset = 0.5 * rng.standard_normal()
         out[q] = (90.0 + 12.0 * (scale * s + offset)).astype(np.float32)
     return out
+
+
+def nanopore_ragged(Z: int, M: int, seed: int, lmin: int, lmax: int, first_query: int = 0):
+    """Variable-length reads (read-until style): lengths log-uniform in
+    [lmin, lmax], each read generated as nanopore_queries would.  Returns (Q concatenated
+    fp32, offsets int64 [Z+1])."""
+    lens = np.empty(Z, np.int64)
+    for q in range(Z):
+        rng = _rng(seed, 500_000 + first_query + q)
+        lens[q] = int(np.exp(rng.uniform(np.log(lmin), np.log(lmax))))
+    parts = [nanopore_queries(1, int(lens[q]), M, seed, first_query=first_query + q)[0] for q in range(Z)]
+    off = np.zeros(Z + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    return np.concatenate(parts).astype(np.float32), off
 
 
 def nanopore_workload(name: str):
