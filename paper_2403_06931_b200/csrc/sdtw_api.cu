@@ -196,8 +196,19 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     int RS = 1;
     const int RSmin = std::max(4 * K, o.ring > 0 ? (int)o.ring : 512);
     while (RS < RSmin) RS <<= 1;
-    const sdtw::SmemLayout L = dual ? sdtw::smem_layout_q(C, WC, trace, GW, (int)Pd, RS)
-                                    : sdtw::smem_layout(C, WC, trace, GW, (int)Pd, RS);
+    auto layout = [&](int rs) {
+        return dual ? sdtw::smem_layout_q(C, WC, trace, GW, (int)Pd, rs) : sdtw::smem_layout(C, WC, trace, GW, (int)Pd, rs);
+    };
+    sdtw::SmemLayout L = layout(RS);
+    // long queries: the query rows and the boundary ring grow with N; shallower inter-warp
+    // rings (down to 4K) when that keeps one more CTA resident per SM
+    if (o.ring <= 0) {
+        auto ctas = [&](int bytes) { return (int)((228 * 1024) / (bytes + 1024)); };
+        for (int rs = RS / 2; rs >= std::max(4 * K, 64); rs /= 2) {
+            const sdtw::SmemLayout L2 = layout(rs);
+            if (ctas(L2.bytes) > ctas(L.bytes) && ctas(L.bytes) < 3) { RS = rs; L = L2; }
+        }
+    }
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
     *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0, dual ? 1 : 0, units, (int)need};
     // Persistent scheduling (default when a cluster is not requested): k resident CTAs
