@@ -104,3 +104,11 @@ def test_oracle_not_imported_by_product():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "sdtw_oracle" not in txt, f
+
+
+def test_gsps_metric_matches_spec_fixture():
+    """Eq. 3 as SPEC's worked example: 1,024,000 floats in 1000 ms -> 0.001024 Gsps."""
+    import json
+    import bench
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "gsps_example.json")))
+    assert abs(bench.gsps(g["floats"], g["ms"]) - g["gsps"]) < 1e-12
