@@ -311,6 +311,9 @@ struct Partial { float cost; int col; int start; int pad; };
 // so diag/left (column w-1) and up (column w) of one chain sit in opposite banks.
 // The query pair is swapped for odd columns by a free FADD2 operand swizzle (.LO_HI)
 // and the reference pairs are stored in their column's orientation.
+#ifndef SDTW_FAST_RUNS
+#define SDTW_FAST_RUNS 1
+#endif
 #ifndef SDTW_FAST_PERIODS
 #define SDTW_FAST_PERIODS 1
 #endif
@@ -838,6 +841,103 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         // row 0 (round transition) or row N-1 (last-row fold) inside it ->
         // warp-uniform, branch-free steps; otherwise U per-lane slow steps.
 #pragma unroll 1
+#if SDTW_FAST_RUNS
+        // Runs of fast periods: one decision per run (the rows of this warp's lanes stay
+        // inside the round and off row N-1 for nf periods), then nf rotation periods of
+        // the same unrolled body with the ring / row pointers advanced per period.
+        for (int s = 0; s < K;) {
+            const int tg = t0 + s;
+            const int lo = rw - (32 * C - 1);
+            int nf = 0;
+            if (lo > 0) {
+                const int lim = (lo > Nm1) ? Pd : Nm1;      // first row the window must not reach
+                nf = min((lim - rw) / PS, (K - s) / PS);
+            }
+            if (nf > 0) {
+                const bool inf_in = gw == 0 && pw == 0 && pa == 0;
+#pragma unroll 1
+                for (int f = 0; f < nf; ++f) {
+                    const int tp = tg + f * PS;
+                    const E* ib0;
+                    const E* ib1;
+                    if (gw == 0) {
+                        ib0 = inf_in ? infs : bnd + rw + f * PS;
+                        ib1 = ib0 + 1;
+                    } else {
+                        ib0 = my_in + ((tp - 1) & (RS - 1));
+                        ib1 = my_in + (tp & (RS - 1));
+                    }
+                    E* ob = has_succ_ring ? succ_ring + (tp & (RS - 1)) : succ_ring + lo + f * PS;
+                    static_for<0, PS>([&](auto hc) {
+                        constexpr int h = decltype(hc)::value;
+                        float lin = __shfl_up_sync(FULL, ls.right[C - 1], 1);
+                        int lins = 0;
+                        if constexpr (TRACE) lins = __shfl_up_sync(FULL, ls.right_s[C - 1], 1);
+                        const E e = (h == 0) ? ib0[0] : ib1[h - 1];
+                        if (lane == 0) {
+                            lin = e.d;
+                            if constexpr (TRACE) lins = e.s;
+                        }
+                        const XRow<C> x = load_xrow_fast<C, h>(xb);
+                        row_cells<C, WC, FMA, TRACE, h % U>(R, Y, x, lin, lins, ls);
+                        if (lane == 31) {
+                            E o;
+                            o.d = ls.right[C - 1];
+                            if constexpr (TRACE) o.s = ls.right_s[C - 1];
+                            ob[h] = o;
+                        }
+                    });
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) xb[j] += (PS / NC) * XC;
+                }
+                b0 += nf * PS;
+                r0 += nf * PS;                               // may land exactly on the next round
+                if (r0 >= Pd) { r0 -= Pd; ++p0; }
+                s += nf * PS;
+                rw += nf * PS;
+                if (rw >= Pd) { rw -= Pd; ++pw; }
+            } else {
+                const int hi = rw + PS - 1;
+                const bool hit0 = lo <= 0 || hi >= Pd;
+                    if (hit0) {                                  // a transition reads the staged strips
+                        asm volatile("cp.async.wait_all;" ::: "memory");
+                        __syncwarp();
+                    }
+#if SDTW_STATIC_SLOW
+                    // unrolled with compile-time rotation (no register moves)
+                    static_for<0, PS>([&](auto hc) {
+                        slow_step(std::integral_constant<int, decltype(hc)::value % U>{}, tg + decltype(hc)::value);
+                        __syncwarp();
+                    });
+#else
+                    // SK steps with compile-time rotation per iteration, then one register
+                    // shuffle back to offset 0 (SK divides U)
+                    constexpr int SK = (SDTW_SLOW_UNROLL < U) ? SDTW_SLOW_UNROLL : U;
+                    static_assert(SDTW_ALT_ORIENT != 2 || C == 1 || (SK % 2 == 0 && U % 2 == 0),
+                                  "diagonal orientation needs even rotation groups");
+#pragma unroll 1
+                    for (int h = 0; h < PS; h += SK) {
+                        static_for<0, SK>([&](auto hc) {
+                            slow_step(hc, tg + h + decltype(hc)::value);
+                            __syncwarp();                    // reconverge before the next step's SHFL
+                        });
+                        unrotate<SK, C, WC, TRACE>(R);
+                    }
+#endif
+                reset_xb();
+                s += PS;
+                rw += PS;
+                if (rw >= Pd) { rw -= Pd; ++pw; }
+            }
+            // the last lane of this warp has entered round pf_round: stage round pf_round+1
+            if (t0 + s > stage_t && pf_round + 1 < Pl) {
+                ++pf_round;
+                stage_t += Pd;
+                __syncwarp();
+                stage_round<C, WC>(ystage, P.Y, P.Malloc, P.Pr, V, u_min, pa + pf_round, lane);
+            }
+        }
+#else
         for (int s = 0; s < K; s += PS) {
             const int tg = t0 + s;
             const int lo = rw - (32 * C - 1), hi = rw + PS - 1;
@@ -923,6 +1023,8 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                 stage_round<C, WC>(ystage, P.Y, P.Malloc, P.Pr, V, u_min, pa + pf_round, lane);
             }
         }
+
+#endif
 
         // ---- publish progress
         __syncwarp();
