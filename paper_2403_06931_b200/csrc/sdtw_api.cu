@@ -183,7 +183,9 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // chunk: 64 steps when the query is long enough that the round period stays N
     // (Pd >= V + (G+1)K), else 32 (r01 sweep: K=64 +1.5% over 32, K=128 -12%)
     const int64_t Nk = rg ? rg->nmin : N;                // ragged: the shortest query decides
-    const int Kreq = o.chunk > 0 ? o.chunk : (Nk >= V + (int64_t)(G + 1) * 64 ? 64 : 32);
+    // (with fast runs, r01: K=128 +1.5 % over 64 at 10M, +1 % at 1M; 256 -10 %)
+    const int Kreq = o.chunk > 0 ? o.chunk
+                                 : (Nk >= V + (int64_t)(G + 1) * 128 ? 128 : (Nk >= V + (int64_t)(G + 1) * 64 ? 64 : 32));
     const int KU = (dual ? 1 : SDTW_FAST_PERIODS) * U;   // chunk = whole fast/slow decision windows
     const int K = KU * std::max(1, (Kreq + KU / 2) / KU);
     const int64_t need = V + (int64_t)(G + 1) * K;
@@ -194,7 +196,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // inter-warp ring depth: deep enough to absorb one warp's round-transition
     // (slow) chunks without stalling its neighbours
     int RS = 1;
-    const int RSmin = std::max(4 * K, o.ring > 0 ? (int)o.ring : 512);
+    const int RSmin = std::max(o.ring > 0 ? 4 * K : 8 * K, o.ring > 0 ? (int)o.ring : 512);
     while (RS < RSmin) RS <<= 1;
     auto layout = [&](int rs) {
         return dual ? sdtw::smem_layout_q(C, WC, trace, GW, (int)Pd, rs) : sdtw::smem_layout(C, WC, trace, GW, (int)Pd, rs);
