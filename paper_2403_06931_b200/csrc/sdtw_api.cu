@@ -184,10 +184,29 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // (Pd >= V + (G+1)K), else 32 (r01 sweep: K=64 +1.5% over 32, K=128 -12%)
     const int64_t Nk = rg ? rg->nmin : N;                // ragged: the shortest query decides
     // (with fast runs, r01: K=128 +1.5 % over 64 at 10M, +1 % at 1M; 256 -10 %)
-    const int Kreq = o.chunk > 0 ? o.chunk
-                                 : (Nk >= V + (int64_t)(G + 1) * 128 ? 128 : (Nk >= V + (int64_t)(G + 1) * 64 ? 64 : 32));
+    // Start-index runs are ALU-pipe bound and their units are short: smaller chunks
+    // measured better there (r01 C5 sweep: N=500 K=32 2.86 vs K=64 2.43; N=1000 K=64 3.14 vs
+    // K=128 2.80; N>=4000 K=128 ~ K=64).
+    int Kauto = Nk >= V + (int64_t)(G + 1) * 128 ? 128 : (Nk >= V + (int64_t)(G + 1) * 64 ? 64 : 32);
+    if (trace) Kauto = std::min(Kauto, Nk <= 600 ? 32 : (Nk <= 2000 ? 64 : 128));
+    const int Kreq = o.chunk > 0 ? o.chunk : Kauto;
     const int KU = (dual ? 1 : SDTW_FAST_PERIODS) * U;   // chunk = whole fast/slow decision windows
-    const int K = KU * std::max(1, (Kreq + KU / 2) / KU);
+    int K = KU * std::max(1, (Kreq + KU / 2) / KU);
+    // long queries: rows and boundary ring fill the shared memory; a shorter chunk allows a
+    // shallower ring (>= 4K) -- take it when that keeps more CTAs resident
+    if (o.chunk <= 0 && o.ring <= 0 && !dual) {
+        auto bytes_for = [&](int k) {
+            const int64_t nd = V + (int64_t)(G + 1) * k;
+            const int pd = (int)(N > nd ? N : nd);
+            int rs = 1;
+            while (rs < std::max(4 * k, 64)) rs <<= 1;
+            return sdtw::smem_layout(C, WC, trace, GW, pd, rs).bytes;
+        };
+        auto ctas = [&](int bytes) { return (int)((228 * 1024) / (bytes + 1024)); };
+        const int base = ctas(bytes_for(K));
+        for (int k = K / 2; base < 3 && k >= 2 * KU; k /= 2)
+            if (ctas(bytes_for(k)) > base) { K = k; break; }
+    }
     const int64_t need = V + (int64_t)(G + 1) * K;
     const int64_t Pd = N > need ? N : need;
     const int64_t Pr = (ctx.M + V * WC - 1) / (V * WC);
