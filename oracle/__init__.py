@@ -44,6 +44,8 @@ def lib():
         L.oracle_walkback.restype = i64
         L.oracle_walkback_path.argtypes = [f32p, i64, i64, i64, i64p, i64p]
         L.oracle_walkback_path.restype = ctypes.c_int
+        L.oracle_round_half.argtypes = [ctypes.c_double, ctypes.c_double]
+        L.oracle_round_half.restype = ctypes.c_float
         L.oracle_znorm.argtypes = [f32p, i64, i64, f32p]
         L.oracle_znorm.restype = ctypes.c_int
         _lib = L
@@ -60,8 +62,9 @@ def _i64(a):
 
 
 def sdtw(Q, Y, fma: bool = True, start: bool = False, last_rows: bool = False,
-         threads: int | None = None):
+         threads: int | None = None, half: bool = False):
     """Batched sDTW on raw inputs (no normalisation). Q: [Z,N] or [N]; Y: [M].
+    half=True: the packed-half recurrence (inputs rounded to binary16, every op rounded).
 
     Returns dict(cost[Z] f32, end[Z] i64, start[Z] i64 | None, last_rows[Z,M] | None)."""
     Q = np.asarray(Q, dtype=np.float32)
@@ -77,7 +80,7 @@ def sdtw(Q, Y, fma: bool = True, start: bool = False, last_rows: bool = False,
     lr = np.empty((Z, M), np.float32) if last_rows else None
     if threads is None:
         threads = os.cpu_count() or 1
-    rc = lib().oracle_sdtw(qp, Z, N, yp, M, int(bool(fma)),
+    rc = lib().oracle_sdtw(qp, Z, N, yp, M, 2 if half else int(bool(fma)),
                            cost.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), _i64(end),
                            _i64(st) if st is not None else None,
                            lr.ctypes.data_as(ctypes.POINTER(ctypes.c_float)) if lr is not None else None,
@@ -105,6 +108,11 @@ def walkback(D, end: int) -> int:
     Dc, dp = _f32(D)
     N, M = Dc.shape
     return int(lib().oracle_walkback(dp, N, M, int(end)))
+
+
+def round_half(v: float, err: float = 0.0) -> float:
+    """binary16 round-to-nearest-even of v (+ an exact residual err), as a float."""
+    return float(lib().oracle_round_half(float(v), float(err)))
 
 
 def walkback_path(D, end: int):

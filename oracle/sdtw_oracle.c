@@ -28,6 +28,9 @@
  *  reading G4/G6): S(0,j) = j; otherwise S(i,j) = S of the predecessor that
  *  attains m, priority diag > up > left on exact equality.
  *
+ *  Packed half (fma_mode == 2): the same recurrence with every value
+ *  rounded to binary16 after each operation (oracle_round_half / oracle_cell16 below).
+ *
  *  Normaliser, §5.1 Eq. 2 and the quoted code:
  *      mean = sum/n; var = sumSq/n - mean*mean; S = sqrt(var); z = (x-mean)/S
  *  population variance (reading G7), fp64 accumulation, one rounding to fp32
@@ -55,6 +58,46 @@ static float oracle_cell(float x, float y, float m, int fma_mode)
         return fmaf(t, t, m);
     float sq = t * t;
     return sq + m;
+}
+
+/* ---------------------------------------------------------------- packed half
+ * SURVEY.md §8(f) NEXT-1, the paper's own precision (the fp32 queries and
+ * reference are converted to float16 and processed as __half2 pairs; P:L108 __hmin2).
+ * Every operation rounds to binary16 (SPEC S1: "rounds after every add/min/FMA"):
+ *     x, y = half(x32), half(y32);  t = half(x - y);  D = half(t*t + m)  (one rounding,
+ *     the HFMA2 of the GPU path; min is exact).
+ * oracle_round_half: IEEE round-to-nearest-even to binary16 of the exact value v + err
+ * (err = the exact residual of a double operation, |err| <= half a double ulp of v;
+ * it only breaks exact ties), returned as a float (binary16 values are exact in fp32).
+ * Overflow goes to +-inf, subnormals are kept. */
+float oracle_round_half(double v, double err)
+{
+    if (v != v) return NAN;
+    const double a = fabs(v);
+    if (a == 0.0) return (float)v;
+    int e;
+    frexp(a, &e);                                      /* a in [2^(e-1), 2^e) */
+    const double ulp = (e - 1 >= -14) ? ldexp(1.0, e - 11) : ldexp(1.0, -24);
+    const double q = a / ulp;                          /* exact: power-of-two scaling */
+    const double fl = floor(q), frac = q - fl;
+    const double errp = (v > 0) ? err : -err;
+    int up;
+    if (frac > 0.5) up = 1;
+    else if (frac < 0.5) up = 0;
+    else up = (errp > 0) || (errp == 0 && fmod(fl, 2.0) == 1.0);
+    const double r = (up ? fl + 1.0 : fl) * ulp;
+    const double out = (r > 65504.0) ? INFINITY : r;
+    return (float)((v < 0) ? -out : out);
+}
+
+static float oracle_cell16(float x, float y, float m)
+{
+    const float t = oracle_round_half((double)x - (double)y, 0.0);  /* exact in double */
+    const double p = (double)t * (double)t;                          /* exact: 22 bits */
+    const double s = p + (double)m;
+    const double bb = s - p;                                         /* TwoSum residual */
+    const double err = (p - (s - bb)) + ((double)m - bb);
+    return oracle_round_half(s, err);
 }
 
 static float min3(float diag, float up, float left)
@@ -88,7 +131,8 @@ static void oracle_one(const float* X, int64_t N, const float* Y, int64_t M,
                 diag = prev[i - 1]; s_diag = sprev[i - 1]; /* +inf at j == 0 */
             }
             float m = min3(diag, up, left);
-            float v = oracle_cell(X[i], Y[j], m, fma_mode);
+            float v = (fma_mode == 2) ? oracle_cell16(oracle_round_half(X[i], 0.0), oracle_round_half(Y[j], 0.0), m)
+                                      : oracle_cell(X[i], Y[j], m, fma_mode);
             int64_t s;
             if (i == 0) s = j;
             else if (diag == m) s = s_diag;
