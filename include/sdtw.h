@@ -62,8 +62,14 @@ enum {
     SDTW_OPT_SCHED = 11,    /* 0 auto; 1 one CTA (or cluster) per query; 2 persistent CTAs pulling
                                (query, round-segment) units -- balances any Z over the SMs */
     SDTW_OPT_SEGMENTS = 12, /* round segments per query under persistent scheduling; 0 = auto */
-    SDTW_OPT_WORKERS = 13   /* resident CTAs per SM under persistent scheduling; 0 = auto
+    SDTW_OPT_WORKERS = 13,  /* resident CTAs per SM under persistent scheduling; 0 = auto
                                (min(occupancy, n_queries / #SMs)) */
+    SDTW_OPT_PRECISION = 14 /* 32 (default): fp32 cells, bit-exact with the fp32 oracle;
+                               16: packed half (the paper's __half2):
+                               queries/reference rounded to binary16, every cell op rounded to
+                               binary16 (HADD2, HFMA2, 3-input half2 min); costs overflow to
+                               +inf above 65504; sdtw_batch / sdtw_batch_ragged only
+                               (no start index), no clusters, OPT_PACKED ignored, W in {30, 62} */
 };
 
 /* Install the reference Y[M] on the current device (copied into a

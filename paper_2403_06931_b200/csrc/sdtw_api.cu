@@ -8,6 +8,7 @@
 #include "sdtw_dp.cuh"
 #include "sdtw_dp_pick.h"
 #include "sdtw_dpq.cuh"
+#include "sdtw_dp16.cuh"
 #include "sdtw_path.cuh"
 #include "sdtw_prep.cuh"
 
@@ -37,6 +38,7 @@ struct Options {
     int sched = 0;       // 0 auto, 1 one CTA (or cluster) per query, 2 persistent segments
     int segments = 0;
     int workers = 0;     // resident CTAs per SM under persistent scheduling (0 = auto)
+    int precision = 32;  // 32 fp32 cells; 16 packed half (sdtw_dp16.cuh)
     cudaStream_t stream = 0;
 };
 Options g_opt;
@@ -133,7 +135,8 @@ using sdtw::DpParams;
 using sdtw::DpKernel;
 
 // dual: the dual-query kernel (two queries per lane, C chains of scalar-y strips)
-DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl, bool dual = false) {
+DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl, bool dual = false, bool half = false) {
+    if (half) return (C == 2 && !trace && !cl && !dual) ? sdtw::pick_dp16(WC) : nullptr;
     if (dual) {
         if (cl) return nullptr;
         return C == 1 ? sdtw::pick_dpq_c1(WC, fma, trace) : (C == 2 ? sdtw::pick_dpq_c2(WC, fma, trace) : nullptr);
@@ -147,6 +150,7 @@ struct LaunchCfg {
     int dual;        // two queries per lane (chains per lane = C)
     int64_t units;   // rings per batch: queries, or query pairs when dual
     int need;        // V + (G+1)K: smallest ring-safe round period (ragged batches: per query)
+    int half;        // packed-half kernel (SDTW_OPT_PRECISION = 16)
 };
 
 // Ragged batch descriptor (host): offsets[Z+1], the longest and shortest query.
@@ -162,13 +166,16 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // auto: two packed chains (f32x2) for cost/end; scalar strips for the start-index
     // variant, whose per-cell start selects double the registers per slot (r01 sweep at
     // N=1000: scalar W=15 3.00, packed W=14 2.89, packed W=30 1.80 TCUPS)
-    const int packed = o.packed < 0 ? (trace ? 0 : 1) : o.packed;
+    const bool half = o.precision == 16;
+    if (half && trace) return fail(SDTW_E_ARG, "the packed-half precision has no start index (OPT_PRECISION=32)");
+    if (half && o.cluster > 1) return fail(SDTW_E_ARG, "the packed-half precision runs without clusters");
+    const int packed = half ? 1 : (o.packed < 0 ? (trace ? 0 : 1) : o.packed);
     const bool dual = packed >= 3;
     int C = dual ? (packed == 3 ? 2 : 1) : (packed == 0 ? 1 : (packed == 1 ? 2 : 4));
     int W = o.segment_w > 0 ? o.segment_w : (C == 4 ? 28 : (C == 2 ? 30 : 15));
     if (W % C != 0) return fail(SDTW_E_ARG, "segment width must be a multiple of the chains per lane");
     int WC = W / C;
-    if (!pick_kernel(C, WC, true, false, false, dual))
+    if (!pick_kernel(C, WC, true, false, false, dual, half))
         return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) + " for this chain layout" +
                                     (C == 4 ? " (28)" : C == 2 ? " (14, 30)" : " (7, 15)"));
     const int64_t units = dual ? (Z + 1) / 2 : Z;
@@ -200,7 +207,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
             const int pd = (int)(N > nd ? N : nd);
             int rs = 1;
             while (rs < std::max(4 * k, 64)) rs <<= 1;
-            return sdtw::smem_layout(C, WC, trace, GW, pd, rs).bytes;
+            return half ? sdtw::smem_layout16(WC, GW, pd, rs).bytes : sdtw::smem_layout(C, WC, trace, GW, pd, rs).bytes;
         };
         auto ctas = [&](int bytes) { return (int)((228 * 1024) / (bytes + 1024)); };
         const int base = ctas(bytes_for(K));
@@ -218,6 +225,12 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     const int RSmin = std::max(o.ring > 0 ? 4 * K : 8 * K, o.ring > 0 ? (int)o.ring : 512);
     while (RS < RSmin) RS <<= 1;
     auto layout = [&](int rs) {
+        if (half) {
+            const sdtw::SmemLayout16 l = sdtw::smem_layout16(WC, GW, (int)Pd, rs);
+            sdtw::SmemLayout r;
+            r.bytes = l.bytes;
+            return r;
+        }
         return dual ? sdtw::smem_layout_q(C, WC, trace, GW, (int)Pd, rs) : sdtw::smem_layout(C, WC, trace, GW, (int)Pd, rs);
     };
     sdtw::SmemLayout L = layout(RS);
@@ -231,7 +244,8 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
         }
     }
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
-    *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0, dual ? 1 : 0, units, (int)need};
+    *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0, dual ? 1 : 0, units, (int)need,
+                     half ? 1 : 0};
     // Persistent scheduling (default when a cluster is not requested): k resident CTAs
     // per SM, k = min(occupancy, rings / SMs), pull (ring, round-segment) units, so every
     // SM carries the same load whatever the batch size mod #SMs is.
@@ -239,7 +253,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     if (sched == 2 || (sched == 0 && CL == 1 && units >= ctx.sms && Pr >= 8)) {
         if (CL != 1) return fail(SDTW_E_ARG, "persistent scheduling needs cluster = 1");
         int occ = 0;
-        DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false, dual);
+        DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false, dual, half);
         cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32 * GW, L.bytes) != cudaSuccess || occ < 1) {
             cudaGetLastError();
@@ -261,7 +275,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
 }
 
 sdtw_status launch_dp(const LaunchCfg& c, bool fma, bool trace, const DpParams& p, cudaStream_t st) {
-    DpKernel k = pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0);
+    DpKernel k = pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0, c.half != 0);
     CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem));
     if (c.CL > 8) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t lc;
@@ -468,7 +482,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.bnd_g = nullptr;
     p.cand = nullptr;
     if (cfg.persistent) {
-        const size_t ent = (trace ? 8 : 4) * (cfg.dual ? 2 : 1);
+        const size_t ent = cfg.half ? 2 : (trace ? 8 : 4) * (cfg.dual ? 2 : 1);
         const size_t R = (size_t)cfg.units;
         const size_t done_b = ((sizeof(int) * R + 255) / 256) * 256;
         const size_t nb = 256 + done_b + 16 * (size_t)Z * cfg.S + ent * R * cfg.Pd;
@@ -774,6 +788,7 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_SCHED: if (v < 0 || v > 2) break; g_opt.sched = (int)v; return SDTW_OK;
         case SDTW_OPT_SEGMENTS: if (v < 0 || v > 4096) break; g_opt.segments = (int)v; return SDTW_OK;
         case SDTW_OPT_WORKERS: if (v < 0 || v > 32) break; g_opt.workers = (int)v; return SDTW_OK;
+        case SDTW_OPT_PRECISION: if (v != 16 && v != 32) break; g_opt.precision = (int)v; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
     return fail(SDTW_E_ARG, "bad value for option " + std::to_string(key));
@@ -796,6 +811,7 @@ sdtw_status sdtw_get_option(int key, int64_t* v) {
         case SDTW_OPT_SCHED: *v = g_opt.sched; return SDTW_OK;
         case SDTW_OPT_SEGMENTS: *v = g_opt.segments; return SDTW_OK;
         case SDTW_OPT_WORKERS: *v = g_opt.workers; return SDTW_OK;
+        case SDTW_OPT_PRECISION: *v = g_opt.precision; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
 }

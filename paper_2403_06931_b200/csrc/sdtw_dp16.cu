@@ -1,0 +1,13 @@
+// sdtw_dp16.cu -- instantiations of the packed-half DP kernel.
+#include "sdtw_dp_pick.h"
+#include "sdtw_dp16.cuh"
+
+namespace sdtw {
+DpKernel pick_dp16(int WC) {
+    switch (WC) {
+        case 15: return sdtw_dp16_kernel<15>;
+        case 31: return sdtw_dp16_kernel<31>;
+        default: return nullptr;
+    }
+}
+}  // namespace sdtw
