@@ -37,7 +37,7 @@ sys.path.insert(0, ROOT)
 
 # ALU roofline: SMs x 128 FP32 lanes x f_SM / (SASS issue slots per cell)
 LANES_PER_SM = 128
-SASS_PER_CELL = {"packed_fma": 2.0, "scalar_fma": 3.0, "scalar_nofma": 4.0, "packed_nofma": 3.5,
+SASS_PER_CELL = {"half2": 1.5, "packed_fma": 2.0, "scalar_fma": 3.0, "scalar_nofma": 4.0, "packed_nofma": 3.5,
                  "packed_fma_trace": 6.0, "scalar_fma_trace": 7.0}
 
 
@@ -209,6 +209,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--half", action="store_true",
+                    help="packed-half precision (SDTW_OPT_PRECISION=16, SURVEY NEXT-1: the paper's __half2)")
     ap.add_argument("--path", action="store_true",
                     help="step = sdtw_path (start index + full warp path, SURVEY NEXT-2)")
     args = ap.parse_args()
@@ -232,6 +234,8 @@ def main():
 
     import paper_2403_06931_b200 as sd
     from paper_2403_06931_b200.distributed import distributed_batch
+    if args.half:
+        sd.set_option(sd.OPT_PRECISION, 16)
 
     Q, Y, w = _workload(args.config, rank, world, args.scaling)
     N, M = w["N"], w["M"]
@@ -295,7 +299,7 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     popt = sd.get_option(sd.OPT_PACKED)
     packed = popt > 0 or (popt < 0 and not trace)          # the library's auto choice (sdtw_api.cu plan)
-    mix = ("packed" if packed else "scalar") + "_fma" + ("_trace" if trace else "")
+    mix = "half2" if args.half else ("packed" if packed else "scalar") + "_fma" + ("_trace" if trace else "")
     k = SASS_PER_CELL[mix]
     peak = sms * LANES_PER_SM * fmax * 1e6 / k / 1e9
     peak3 = sms * LANES_PER_SM * fmax * 1e6 / 3.0 / 1e9
@@ -357,7 +361,7 @@ def main():
         line = {
             "metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f16" if args.half else "f32",
             "data": "synthetic nanopore-like signals (datagen, seeded); random reference, no trained weights",
             "config": {"workload": "%s: %d x %d queries vs %d-sample reference%s" % (
                 args.config, w["Z"], N, M, " (start index on)" if trace else ""),
