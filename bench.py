@@ -48,14 +48,15 @@ def gsps(floats: float, ms: float) -> float:
     return floats / (ms * 1e9 / 1000.0)
 
 
-def _traffic(config, w):
+def _traffic(config, w, precision=32):
     """DRAM bytes (read + write) per DP launch from the committed ncu capture of this
     workload (profiles/traffic_<config>.json, written by scripts/ncu_traffic.py from
     `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum`), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic_%s.json" % config)) as f:
             t = json.load(f)
-        if int(t["Z"]) == int(w["Z_local"]) and int(t["N"]) == w["N"] and int(t["M"]) == w["M"]:
+        if (int(t["Z"]) == int(w["Z_local"]) and int(t["N"]) == w["N"] and int(t["M"]) == w["M"]
+                and int(t.get("precision", 32)) == precision):
             return float(t["dram_bytes_per_launch"])
     except Exception:
         pass
@@ -307,7 +308,7 @@ def main():
     achieved = (w["cells_local"] if ragged else float(w["Z_local"]) * N * M) / (dp_avg / 1e3) / 1e9
     clocks = sampler.summary()
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "GCUPS", "frac": achieved / peak,
-            "traffic": _traffic(args.config, w), "sass_per_cell": k, "peak_source": "%s sm_max_mhz=%.0f x %d SMs x %d lanes / %g"
+            "traffic": _traffic(args.config, w, 16 if args.half else 32), "sass_per_cell": k, "peak_source": "%s sm_max_mhz=%.0f x %d SMs x %d lanes / %g"
             % (src, fmax, sms, LANES_PER_SM, k),
             "headline_peak_k3": peak3, "headline_frac_k3": achieved / peak3,
             "dp_kernel_ms": dp_avg}

@@ -15,7 +15,7 @@ for r in rows[hi + 1:]:
         vals[r[mn]] = float(r[mv].replace(",", "")) * scale.get(r[mu], 1)
     if "sdtw_dp" in r[kn] and r[mn] == "gpu__time_duration.sum":
         vals["time_" + r[mu]] = float(r[mv].replace(",", ""))
-out = {"config": config, "Z": int(Z), "N": int(N), "M": int(M),
+out = {"config": config, "Z": int(Z), "N": int(N), "M": int(M), "precision": 32,
        "dram_bytes_read": vals.get("dram__bytes_read.sum"), "dram_bytes_write": vals.get("dram__bytes_write.sum"),
        "dram_bytes_per_launch": vals.get("dram__bytes_read.sum", 0) + vals.get("dram__bytes_write.sum", 0),
        "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (one DP launch of bench.py --config %s)" % config}
