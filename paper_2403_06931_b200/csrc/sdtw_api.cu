@@ -135,8 +135,10 @@ using sdtw::DpParams;
 using sdtw::DpKernel;
 
 // dual: the dual-query kernel (two queries per lane, C chains of scalar-y strips)
-DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl, bool dual = false, bool half = false) {
+DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl, bool dual = false, bool half = false,
+                     bool xs = false) {
     if (half) return (C == 2 && !trace && !cl && !dual) ? sdtw::pick_dp16(WC) : nullptr;
+    if (xs) return (C == 2 && !trace && !cl && !dual) ? sdtw::pick_dp_c2xs(WC, fma) : nullptr;
     if (dual) {
         if (cl) return nullptr;
         return C == 1 ? sdtw::pick_dpq_c1(WC, fma, trace) : (C == 2 ? sdtw::pick_dpq_c2(WC, fma, trace) : nullptr);
@@ -151,6 +153,7 @@ struct LaunchCfg {
     int64_t units;   // rings per batch: queries, or query pairs when dual
     int need;        // V + (G+1)K: smallest ring-safe round period (ragged batches: per query)
     int half;        // packed-half kernel (SDTW_OPT_PRECISION = 16)
+    int xs;          // single-row query layout (long queries)
 };
 
 // Ragged batch descriptor (host): offsets[Z+1], the longest and shortest query.
@@ -244,8 +247,16 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
         }
     }
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
+    // long queries: the single-row layout halves the rows' bytes; take it when that keeps
+    // one more CTA resident (C == 2, cost/end, no cluster)
+    bool xs = false;
+    if (!half && !dual && !trace && C == 2 && CL == 1 && pick_kernel(C, WC, true, false, false, false, false, true)) {
+        auto ctas = [&](int bytes) { return (int)((228 * 1024) / (bytes + 1024)); };
+        const sdtw::SmemLayout Lx = sdtw::smem_layout(C, WC, trace, GW, (int)Pd, RS, true);
+        if (ctas(L.bytes) < 3 && ctas(Lx.bytes) > ctas(L.bytes)) { L = Lx; xs = true; }
+    }
     *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0, dual ? 1 : 0, units, (int)need,
-                     half ? 1 : 0};
+                     half ? 1 : 0, xs ? 1 : 0};
     // Persistent scheduling (default when a cluster is not requested): k resident CTAs
     // per SM, k = min(occupancy, rings / SMs), pull (ring, round-segment) units, so every
     // SM carries the same load whatever the batch size mod #SMs is.
@@ -253,7 +264,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     if (sched == 2 || (sched == 0 && CL == 1 && units >= ctx.sms && Pr >= 8)) {
         if (CL != 1) return fail(SDTW_E_ARG, "persistent scheduling needs cluster = 1");
         int occ = 0;
-        DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false, dual, half);
+        DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false, dual, half, xs);
         cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32 * GW, L.bytes) != cudaSuccess || occ < 1) {
             cudaGetLastError();
@@ -275,7 +286,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
 }
 
 sdtw_status launch_dp(const LaunchCfg& c, bool fma, bool trace, const DpParams& p, cudaStream_t st) {
-    DpKernel k = pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0, c.half != 0);
+    DpKernel k = pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0, c.half != 0, c.xs != 0);
     CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem));
     if (c.CL > 8) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t lc;

@@ -272,7 +272,9 @@ __host__ __device__ __forceinline__ constexpr int xrow_classes(int C) { return C
 struct SmemLayout {
     int off_ctr, off_red, off_inf, off_x, off_bnd, off_ring, off_stage, bytes;
 };
-__host__ __device__ inline SmemLayout smem_layout(int C, int WC, bool trace, int GW, int Pd, int RS) {
+// xs: "single" row layout (x_r alone, plain row order; C == 2 only): half the bytes per
+// row for long queries whose rows would otherwise cost a resident CTA, one more LDS per step.
+__host__ __device__ inline SmemLayout smem_layout(int C, int WC, bool trace, int GW, int Pd, int RS, bool xs = false) {
     SmemLayout L;
     const int ent = trace ? 8 : 4;
     int o = 0;
@@ -280,7 +282,7 @@ __host__ __device__ inline SmemLayout smem_layout(int C, int WC, bool trace, int
     L.off_red = o;  o += 16 * (32 + 16);                // per-warp + per-rank partials
     L.off_inf = o;  o += 32 * 8;                        // +inf inbox entries (round 0)
     o = (o + 15) & ~15;
-    L.off_x = o;    o += xrow_stride(Pd, xrow_classes(C)) * xrow_classes(C) * xrow_floats(C) * 4;
+    L.off_x = o;    o += xs ? Pd * 4 : xrow_stride(Pd, xrow_classes(C)) * xrow_classes(C) * xrow_floats(C) * 4;
     o = (o + 15) & ~15;
     L.off_bnd = o;  o += Pd * ent;
     o = (o + 15) & ~15;
@@ -389,10 +391,11 @@ template <> struct XRow<1> { float v[1]; };
 template <> struct XRow<2> { unsigned long long p[1]; };
 template <> struct XRow<4> { unsigned long long p[2]; };
 // slow path: samples of row r (any residue)
-template <int C>
+template <int C, bool XS = false>
 __device__ __forceinline__ XRow<C> load_xrow(const float* xs, int r, int Pd) {
     XRow<C> x;
     if constexpr (C == 1) x.v[0] = xs[r];
+    else if constexpr (XS) x.p[0] = pk(xs[r], xs[r >= 1 ? r - 1 : r - 1 + Pd]);
     else {
         const unsigned long long* xp = reinterpret_cast<const unsigned long long*>(xs);
         x.p[0] = xp[xrow_index(r, Pd, C)];
@@ -402,10 +405,11 @@ __device__ __forceinline__ XRow<C> load_xrow(const float* xs, int r, int Pd) {
 }
 // fast path: step h of a rotation period starting at row r0, with xb[j] pointing
 // at row r0+j (residue class (r0+j) mod C, j < C); rows stay inside one round
-template <int C, int h>
-__device__ __forceinline__ XRow<C> load_xrow_fast(const float* const (&xb)[xrow_classes(C)]) {
+template <int C, int h, bool XS = false>
+__device__ __forceinline__ XRow<C> load_xrow_fast(const float* const* xb) {
     XRow<C> x;
     if constexpr (C == 1) x.v[0] = xb[0][h];
+    else if constexpr (XS) x.p[0] = pk(xb[0][h], xb[0][h - 1]);    // rows r0+h, r0+h-1 (>= 0 in a fast period)
     else {
         constexpr int j0 = h % C, o0 = h / C;                       // row r0+h
         x.p[0] = reinterpret_cast<const unsigned long long*>(xb[j0])[o0];
@@ -580,8 +584,9 @@ __device__ __forceinline__ int fmod_pos(int a, int m) { int r = a % m; return r 
 __device__ __forceinline__ bool hits_row(int blo, int len, int row, int Pd) { return fmod_pos(row - blo, Pd) < len; }
 
 // ============================================================================ kernel
-template <int C, int WC, bool FMA, bool TRACE, bool CLUSTER>
+template <int C, int WC, bool FMA, bool TRACE, bool CLUSTER, bool XS = false>
 __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2) sdtw_dp_kernel(const DpParams P) {
+    static_assert(!XS || C == 2, "single-row layout is for two chains");
     static_assert(C == 1 || C == 2 || C == 4, "chains per lane");
     static_assert(((WC + 1) & WC) == 0 && (32 * C) % (WC + 1) == 0 && (WC + 1) % C == 0,
                   "rotation period U = WC+1 must be a power of two dividing 32*C and divisible by C");
@@ -601,7 +606,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     const int gw = rank * GW + warp;
     const int V = 32 * C * G;
     const int PdMax = P.Pd, K = P.K, RS = P.RS;
-    const SmemLayout L = smem_layout(C, WC, TRACE, GW, PdMax, RS);
+    const SmemLayout L = smem_layout(C, WC, TRACE, GW, PdMax, RS, XS);
 
     int* pp = reinterpret_cast<int*>(smem + L.off_ctr);        // producer progress seen by warp w
     int* cp = pp + 32;                                          // consumer progress of w's successor
@@ -641,8 +646,8 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     const int u0 = C * (32 * gw + lane);
     const int u_last = V - 1;
 
-    constexpr int XC = xrow_floats(C);
-    constexpr int NC = xrow_classes(C);
+    constexpr int XC = XS ? 1 : xrow_floats(C);
+    constexpr int NC = XS ? 1 : xrow_classes(C);
     int* unit_sh = pp + 64;                                     // broadcast of the grabbed unit
     for (int unit_iter = 0;; ++unit_iter) {
     // ---- which unit: (query q, rounds [pa, pb))
@@ -687,7 +692,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     // segment's last column), counters
     const E* bg = reinterpret_cast<const E*>(P.bnd_g) + (long)q * PdMax;
     for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
-        float* dst = xs + (long)xrow_index(r, Pd, NC) * XC;
+        float* dst = XS ? xs + r : xs + (long)xrow_index(r, Pd, NC) * XC;
 #pragma unroll
         for (int j = 0; j < XC; ++j) {
             int rr = r - j;
@@ -789,7 +794,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
 #pragma unroll
         for (int c = 0; c < C; ++c)
             if (rcs[c] == 0) enter_strip<C, WC, TRACE>(R, Y, c, (long)(pa + pcs[c]) * V + u0 + c, ylane + c * WC, ls, H);
-        const XRow<C> x = load_xrow<C>(xs, r0, Pd);
+        const XRow<C> x = load_xrow<C, XS>(xs, r0, Pd);
         row_cells<C, WC, FMA, TRACE, H>(R, Y, x, lin, lins, ls);
 #pragma unroll
         for (int c = 0; c < C; ++c) {
@@ -821,7 +826,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         for (int j = 0; j < NC; ++j) {
             int rr = r0 + j;
             if (rr >= Pd) rr -= Pd;
-            xb[j] = xs + (long)xrow_index(rr, Pd, NC) * XC;
+            xb[j] = XS ? xs + rr : xs + (long)xrow_index(rr, Pd, NC) * XC;
         }
     };
     reset_xb();
@@ -878,7 +883,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                             lin = e.d;
                             if constexpr (TRACE) lins = e.s;
                         }
-                        const XRow<C> x = load_xrow_fast<C, h>(xb);
+                        const XRow<C> x = load_xrow_fast<C, h, XS>(xb);
                         row_cells<C, WC, FMA, TRACE, h % U>(R, Y, x, lin, lins, ls);
                         if (lane == 31) {
                             E o;
@@ -970,7 +975,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                         lin = e.d;
                         if constexpr (TRACE) lins = e.s;
                     }
-                    const XRow<C> x = load_xrow_fast<C, h>(xb);
+                    const XRow<C> x = load_xrow_fast<C, h, XS>(xb);
                     row_cells<C, WC, FMA, TRACE, h % U>(R, Y, x, lin, lins, ls);
                     if (lane == 31) {
                         E o;

@@ -16,4 +16,9 @@ DpKernel pick_dp_c2(int WC, bool fma, bool cl) {
         default: return nullptr;
     }
 }
+// single-row query layout (long queries, see smem_layout): cost/end, no cluster
+DpKernel pick_dp_c2xs(int WC, bool fma) {
+    if (WC != 15) return nullptr;
+    return fma ? sdtw_dp_kernel<2, 15, true, false, false, true> : sdtw_dp_kernel<2, 15, false, false, false, true>;
+}
 }  // namespace sdtw

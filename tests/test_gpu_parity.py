@@ -269,3 +269,11 @@ def test_deterministic_repeated_runs():
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
             assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.parametrize("fma", [1, 0])
+def test_long_queries_single_row_layout(fma):
+    """N = 8,000: the rows + boundary ring select the single-row query layout (one more
+    resident CTA); bit-exact against the oracle like every other schedule."""
+    Q, Y = _inputs(4, 8000, 20_000, 10)
+    _check_exact(Q, Y, _gpu(Q, Y, OPT_FMA=fma), fma=bool(fma))

@@ -105,3 +105,13 @@ def test_ragged_errors_and_empty():
             assert e.value.status == sd.E_ARG
         c, e = sd.batch_ragged(np.zeros(0, np.float32), np.zeros(1, np.int64))
         assert c.shape == (0,)
+
+
+def test_ragged_long_reads_bit_exact():
+    """Reads up to 9,000 samples (single-row query layout) next to short ones."""
+    lengths = np.array([9000, 120, 4000, 700, 8800, 33])
+    qs, Q, off, Y = _ragged_inputs(lengths, 15_000, 12)
+    with sd.options(OPT_NORMALIZE=0):
+        sd.set_reference(Y)
+        c, e = sd.batch_ragged(Q, off)
+    _check(qs, Y, c, e, None, True)
