@@ -64,6 +64,7 @@ enum {
     SDTW_OPT_SEGMENTS = 12, /* round segments per query under persistent scheduling; 0 = auto */
     SDTW_OPT_WORKERS = 13,  /* resident CTAs per SM under persistent scheduling; 0 = auto
                                (min(occupancy, n_queries / #SMs)) */
+    SDTW_OPT_PAD = 15,      /* extra idle rows per round period (ring slack for long rings); 0 = auto */
     SDTW_OPT_PRECISION = 14 /* 32 (default): fp32 cells, bit-exact with the fp32 oracle;
                                16: packed half (the paper's __half2):
                                queries/reference rounded to binary16, every cell op rounded to

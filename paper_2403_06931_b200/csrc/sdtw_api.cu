@@ -39,6 +39,7 @@ struct Options {
     int segments = 0;
     int workers = 0;     // resident CTAs per SM under persistent scheduling (0 = auto)
     int precision = 32;  // 32 fp32 cells; 16 packed half (sdtw_dp16.cuh)
+    int pad = 0;         // extra idle rows per round period (0 = auto)
     cudaStream_t stream = 0;
 };
 Options g_opt;
@@ -218,7 +219,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
             if (ctas(bytes_for(k)) > base) { K = k; break; }
     }
     const int64_t need = V + (int64_t)(G + 1) * K;
-    const int64_t Pd = N > need ? N : need;
+    const int64_t Pd = std::max<int64_t>(N + o.pad, need);
     const int64_t Pr = (ctx.M + V * WC - 1) / (V * WC);
     if (Pr * Pd + V + 2 * K >= (1LL << 31) || Pr * V * WC >= (1LL << 31))
         return fail(SDTW_E_ARG, "problem too large for 32-bit step/column counters");
@@ -800,6 +801,7 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_SEGMENTS: if (v < 0 || v > 4096) break; g_opt.segments = (int)v; return SDTW_OK;
         case SDTW_OPT_WORKERS: if (v < 0 || v > 32) break; g_opt.workers = (int)v; return SDTW_OK;
         case SDTW_OPT_PRECISION: if (v != 16 && v != 32) break; g_opt.precision = (int)v; return SDTW_OK;
+        case SDTW_OPT_PAD: if (v < 0 || v > (1 << 20)) break; g_opt.pad = (int)v; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
     return fail(SDTW_E_ARG, "bad value for option " + std::to_string(key));
@@ -823,6 +825,7 @@ sdtw_status sdtw_get_option(int key, int64_t* v) {
         case SDTW_OPT_SEGMENTS: *v = g_opt.segments; return SDTW_OK;
         case SDTW_OPT_WORKERS: *v = g_opt.workers; return SDTW_OK;
         case SDTW_OPT_PRECISION: *v = g_opt.precision; return SDTW_OK;
+        case SDTW_OPT_PAD: *v = g_opt.pad; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
 }
