@@ -133,6 +133,10 @@ def _workload(cfg_name: str, rank: int, world: int, scaling: str):
         first = rank * per
         Zl = max(0, min(Z, first + per) - first)
         Zg = Z
+    if cfg.get("cbf"):
+        from datagen import cbf_batch, cbf_reference
+        Q = cbf_batch(Zl, N, seed + 1000 * first)
+        return Q, cbf_reference(M, seed), dict(Z=Zg, Z_local=Zl, N=N, M=M, seed=seed, start=cfg["start"])
     Y = nanopore_reference(M, seed)
     if cfg.get("ragged"):
         from datagen import nanopore_ragged
@@ -153,8 +157,13 @@ def run_reference(args):
     # bounded sample: `threads` queries x N against the first Ms reference samples,
     # sized for ~2-4 s per step at ~0.3 GCUPS per core
     Ms = int(min(cfg["M"], max(2000, 1.0e9 / N)))
-    Y = nanopore_reference(cfg["M"], cfg["seed"])[:Ms]
-    Q = nanopore_queries(threads, N, cfg["M"], cfg["seed"])
+    if cfg.get("cbf"):
+        from datagen import cbf_batch, cbf_reference
+        Y = cbf_reference(cfg["M"], cfg["seed"])[:Ms]
+        Q = cbf_batch(threads, N, cfg["seed"])
+    else:
+        Y = nanopore_reference(cfg["M"], cfg["seed"])[:Ms]
+        Q = nanopore_queries(threads, N, cfg["M"], cfg["seed"])
     Yn = oracle.znorm(Y[None])[0]
     times = []
     for i in range(args.warmup + args.steps):

@@ -44,6 +44,8 @@ CONFIGS = {
     "c5_1000": dict(Z=512, N=1000, M=1_000_000, seed=5, start=True),
     "c5_4000": dict(Z=512, N=4000, M=1_000_000, seed=5, start=True),
     "c5_8000": dict(Z=512, N=8000, M=1_000_000, seed=5, start=True),
+    # the paper's generator family (CBF) at config-2 shape: throughput is data-oblivious
+    "c2_cbf": dict(Z=512, N=2000, M=100_000, seed=2, start=False, cbf=True),
     # NEXT-4: a ragged batch of reads, lengths log-uniform in [500, 8000] (N = mean, info only)
     "c6_ragged": dict(Z=512, N=2700, M=1_000_000, seed=6, start=False, ragged=(500, 8000)),
 }

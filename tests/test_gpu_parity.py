@@ -277,3 +277,11 @@ def test_long_queries_single_row_layout(fma):
     resident CTA); bit-exact against the oracle like every other schedule."""
     Q, Y = _inputs(4, 8000, 20_000, 10)
     _check_exact(Q, Y, _gpu(Q, Y, OPT_FMA=fma), fma=bool(fma))
+
+
+def test_cbf_inputs_bit_exact():
+    """The paper's own test-data family (CBF)."""
+    from datagen import cbf_batch, cbf_reference
+    Y = oracle.znorm(cbf_reference(8000, 2)[None])[0]
+    Q = oracle.znorm(cbf_batch(6, 256, 2))
+    _check_exact(Q, Y, _gpu(Q, Y, trace=True), trace=True)
