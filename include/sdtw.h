@@ -60,11 +60,20 @@ enum {
     SDTW_OPT_PROFILE = 9,   /* 1: time the DP kernel with CUDA events (sdtw_profile) */
     SDTW_OPT_RING = 10,     /* inter-warp hand-off ring entries (rounded up to a power of two); 0 = auto */
     SDTW_OPT_SCHED = 11,    /* 0 auto; 1 one CTA (or cluster) per query; 2 persistent CTAs pulling
-                               (query, round-segment) units -- balances any Z over the SMs */
+                               (query, round-segment) units -- balances any Z over the SMs;
+                               3 speculative segments: every round-segment of a query starts
+                               at once from a +inf boundary, then a short correction pass per
+                               segment boundary repairs the result exactly (cost / end only;
+                               auto for batches smaller than the SM count) */
     SDTW_OPT_SEGMENTS = 12, /* round segments per query under persistent scheduling; 0 = auto */
     SDTW_OPT_WORKERS = 13,  /* resident CTAs per SM under persistent scheduling; 0 = auto
                                (min(occupancy, n_queries / #SMs)) */
     SDTW_OPT_PAD = 15,      /* extra idle rows per round period (ring slack for long rings); 0 = auto */
+    SDTW_OPT_SPEC_ROUNDS = 16, /* speculative segments: rounds of each correction pass (the
+                               columns over which the boundary's paths must be overtaken by
+                               the segment's own); 0 = auto (>= 3 query lengths).  A segment
+                               whose correction is not overtaken in time is recomputed, so
+                               any value gives exact results; it only moves work */
     SDTW_OPT_PRECISION = 14 /* 32 (default): fp32 cells, bit-exact with the fp32 oracle;
                                16: packed half (the paper's __half2):
                                queries/reference rounded to binary16, every cell op rounded to
@@ -134,6 +143,11 @@ sdtw_status sdtw_get_option(int key, int64_t* value);
  * *dp_ms = summed CUDA-event duration of the DP kernel launch(es) on the option
  * stream; *launches = kernels the last call launched (all of them). */
 sdtw_status sdtw_profile(double* dp_ms, int64_t* launches);
+
+/* Speculative segments (SDTW_OPT_SCHED=3, or auto for small batches): *n = queries of the
+ * last sdtw_batch call whose correction pass was not overtaken within OPT_SPEC_ROUNDS
+ * rounds and that were therefore recomputed with sequential segments (0 otherwise). */
+sdtw_status sdtw_spec_recomputed(int64_t* n);
 
 /* Total kernels this process has launched through the library. */
 int64_t sdtw_launch_count(void);

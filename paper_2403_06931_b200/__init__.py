@@ -42,22 +42,24 @@ _lib.sdtw_znormalize.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p]
 _lib.sdtw_set_option.argtypes = [ctypes.c_int, _i64]
 _lib.sdtw_get_option.argtypes = [ctypes.c_int, ctypes.POINTER(_i64)]
 _lib.sdtw_profile.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]
+_lib.sdtw_spec_recomputed.argtypes = [ctypes.POINTER(_i64)]
 _lib.sdtw_launch_count.restype = _i64
 _lib.sdtw_last_error.restype = ctypes.c_char_p
 _lib.sdtw_version.restype = ctypes.c_int
 for _n in ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
-           "sdtw_set_option", "sdtw_get_option", "sdtw_profile"):
+           "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_spec_recomputed"):
     getattr(_lib, _n).restype = ctypes.c_int
 
 # ABI constants (include/sdtw.h)
 OK, E_ARG, E_NOREF, E_CUDA, E_NOMEM, E_NONFINITE = range(6)
 OPT_NORMALIZE, OPT_FMA, OPT_SEGMENT_W, OPT_LANES, OPT_CLUSTER, OPT_STREAM, OPT_PACKED, OPT_CHUNK, \
-    OPT_PROFILE, OPT_RING, OPT_SCHED, OPT_SEGMENTS, OPT_WORKERS, OPT_PRECISION, OPT_PAD = range(1, 16)
+    OPT_PROFILE, OPT_RING, OPT_SCHED, OPT_SEGMENTS, OPT_WORKERS, OPT_PRECISION, OPT_PAD, \
+    OPT_SPEC_ROUNDS = range(1, 17)
 _STATUS = {0: "SDTW_OK", 1: "SDTW_E_ARG", 2: "SDTW_E_NOREF", 3: "SDTW_E_CUDA", 4: "SDTW_E_NOMEM",
            5: "SDTW_E_NONFINITE"}
 
 EXPORTED_SYMBOLS = ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
-                    "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_launch_count",
+                    "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_spec_recomputed", "sdtw_launch_count",
                     "sdtw_last_error", "sdtw_release", "sdtw_version")
 
 
@@ -234,6 +236,13 @@ def profile():
     n = _i64()
     _check(_lib.sdtw_profile(ctypes.byref(ms), ctypes.byref(n)))
     return float(ms.value), int(n.value)
+
+
+def spec_recomputed() -> int:
+    """Queries of the last batch call recomputed after a failed speculative correction."""
+    n = _i64()
+    _check(_lib.sdtw_spec_recomputed(ctypes.byref(n)))
+    return int(n.value)
 
 
 def launch_count() -> int:

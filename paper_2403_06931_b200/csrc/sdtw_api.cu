@@ -40,6 +40,7 @@ struct Options {
     int workers = 0;     // resident CTAs per SM under persistent scheduling (0 = auto)
     int precision = 32;  // 32 fp32 cells; 16 packed half (sdtw_dp16.cuh)
     int pad = 0;         // extra idle rows per round period (0 = auto)
+    int spec_rounds = 0; // speculative segments: rounds per correction pass (0 = auto)
     cudaStream_t stream = 0;
 };
 Options g_opt;
@@ -60,6 +61,9 @@ struct Ctx {
     unsigned char* ws_path = nullptr; size_t ws_path_n = 0;     // sdtw_path codes / row buffers / outputs
     unsigned char* ws_rag = nullptr; size_t ws_rag_n = 0;       // ragged-batch offsets + lengths
     int* order_d = nullptr; size_t order_n = 0;     // unit grab order (device) and its key
+    int4* utab_d = nullptr; size_t utab_n = 0;      // speculative segments: unit-kind table
+    float* ws_fix = nullptr; size_t ws_fix_n = 0;   // speculative segments: recomputed queries
+    int64_t last_fixups = 0;                        // queries recomputed by the last call
     int64_t order_key[3] = {-1, -1, -1};
     int* flag_d = nullptr;
     int* flag_h = nullptr;
@@ -155,6 +159,8 @@ struct LaunchCfg {
     int need;        // V + (G+1)K: smallest ring-safe round period (ragged batches: per query)
     int half;        // packed-half kernel (SDTW_OPT_PRECISION = 16)
     int xs;          // single-row query layout (long queries)
+    int spec = 0;    // speculative segments: Sseg segments, correction passes of Rc rounds
+    int Sseg = 0, Rc = 0;
 };
 
 // Ragged batch descriptor (host): offsets[Z+1], the longest and shortest query.
@@ -262,6 +268,44 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // per SM, k = min(occupancy, rings / SMs), pull (ring, round-segment) units, so every
     // SM carries the same load whatever the batch size mod #SMs is.
     const int sched = o.sched;
+    // Speculative segments: small batches (fewer rings than SMs) cannot
+    // fill the GPU with sequential segments; every segment then starts at once and a
+    // correction pass of Rc rounds per segment boundary restores the exact result.
+    const int64_t cols = V * WC;
+    const int Rc = o.spec_rounds > 0 ? o.spec_rounds : (int)std::max<int64_t>(1, (3 * N + cols - 1) / cols);
+    const bool spec_ok = !trace && !half && !dual && CL == 1 && !rg && Pr >= 4 * (int64_t)(Rc + 1);
+    if (sched == 3 && !spec_ok)
+        return fail(SDTW_E_ARG, "speculative segments need cost/end, fp32, no clusters, fixed-length "
+                                "queries and >= 4 segments of more than OPT_SPEC_ROUNDS rounds");
+    int occ = 0;
+    if (sched == 3 || (sched == 0 && spec_ok)) {
+        DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false, dual, half, xs);
+        cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32 * GW, L.bytes) != cudaSuccess || occ < 1) {
+            cudaGetLastError();
+            return fail(SDTW_E_CUDA, "occupancy query failed");
+        }
+    }
+    // auto: when the rings cannot fill every resident CTA slot (r01 C3 sweep, 10M x 2000:
+    // Z=64 1.88 -> 7.91 TCUPS, Z=200 4.24 -> 7.65, Z=300 7.16 -> 7.67, Z=444 8.46 = 8.48)
+    if (sched == 3 || (sched == 0 && spec_ok && units < (int64_t)occ * ctx.sms)) {
+        const int per_sm = o.workers > 0 ? std::min(o.workers, occ) : occ;
+        const int64_t W = (int64_t)per_sm * ctx.sms;
+        // segments: about four units per worker (Z=64: 7 segments 6.21, 14 7.68, 28 7.91,
+        // 56 7.99 TCUPS), each > Rc rounds and long enough that the correction passes stay
+        // a small share (Rc / segment length)
+        int64_t Sg = o.segments > 0 ? o.segments : (4 * W + units - 1) / units;
+        Sg = std::min<int64_t>(Sg, Pr / std::max<int64_t>(4 * (Rc + 1), 8));
+        Sg = std::max<int64_t>(Sg, 2);
+        if (Pr / Sg <= Rc) return fail(SDTW_E_ARG, "speculative segments shorter than the correction pass");
+        cfg->spec = 1;
+        cfg->Sseg = (int)Sg;
+        cfg->Rc = Rc;
+        cfg->persistent = 1;
+        cfg->S = 3 * (int)Sg - 1;                           // unit kinds per ring (A_s, B_s, C_s)
+        cfg->workers = (int)std::min<int64_t>(W, units * cfg->S);
+        return SDTW_OK;
+    }
     if (sched == 2 || (sched == 0 && CL == 1 && units >= ctx.sms && Pr >= 8)) {
         if (CL != 1) return fail(SDTW_E_ARG, "persistent scheduling needs cluster = 1");
         int occ = 0;
@@ -387,6 +431,115 @@ std::vector<int> unit_order_weighted(int64_t R, int S, int64_t W, const std::vec
 }
 
 sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
+                      int64_t* out_start, bool trace, BatchDev* dev_out, Ragged rg);
+
+// Speculative segments: queries whose correction pass was not overtaken within Rc rounds
+// (fix[q] != 0) are recomputed with sequential segments from their normalised rows and
+// their results replace the speculative ones.
+sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const int* fix_d, float* dc, int64_t* de,
+                       cudaStream_t st) {
+    std::vector<int> fix((size_t)Z);
+    CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fix.data(), fix_d, (size_t)Z * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (*ctx->flag_h) return SDTW_OK;                  // non-finite input: no results (reported by the caller)
+    std::vector<int64_t> idx;
+    for (int64_t q = 0; q < Z; ++q)
+        if (fix[q]) idx.push_back(q);
+    if (idx.empty()) return SDTW_OK;
+    const int64_t F = (int64_t)idx.size();
+    const size_t need = 3 * (size_t)F + (size_t)F * (size_t)N;   // (end, cost) per query + rows
+    sdtw_status s = grow(&ctx->ws_fix, &ctx->ws_fix_n, need);
+    if (s != SDTW_OK) return s;
+    int64_t* fe = reinterpret_cast<int64_t*>(ctx->ws_fix);
+    float* fc = ctx->ws_fix + 2 * F;
+    float* rows = fc + F;
+    for (int64_t k = 0; k < F; ++k)
+        CK(cudaMemcpyAsync(rows + k * N, xd + idx[k] * N, (size_t)N * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    const Options saved = g_opt;
+    g_opt.normalize = 0;
+    g_opt.profile = 0;
+    g_opt.sched = 1;                                  // one CTA per ring: no speculation again
+    g_opt.stream = st;
+    const int64_t fixed_before = F;
+    s = run_batch(rows, F, N, fc, fe, nullptr, false, nullptr, Ragged());
+    g_opt = saved;
+    if (s != SDTW_OK) return s;
+    for (int64_t k = 0; k < F; ++k) {
+        CK(cudaMemcpyAsync(dc + idx[k], fc + k, sizeof(float), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(de + idx[k], fe + k, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    }
+    ctx->last_fixups = fixed_before;
+    return SDTW_OK;
+}
+
+// Speculative segments: the unit-kind table {pa, pb, in_k, db} of one
+// ring -- A_s (k = s): rounds [s*Pr/Sg, +Rc) from a +inf boundary; B_s (k = Sg + s): the
+// rest of segment s after A_s; C_s (k = 2Sg + s - 1, s >= 1): A_s's rounds again from
+// B_{s-1}'s end column with no free start.
+std::vector<int4> spec_table(int Pr, int Sg, int Rc) {
+    std::vector<int4> t(3 * Sg - 1);
+    for (int s = 0; s < Sg; ++s) {
+        const int a = (int)((int64_t)s * Pr / Sg), e = (int)((int64_t)(s + 1) * Pr / Sg);
+        t[s] = make_int4(a, a + Rc, -1, 0);
+        t[Sg + s] = make_int4(a + Rc, e, s, 0);
+        if (s > 0) t[2 * Sg + s - 1] = make_int4(a, a + Rc, Sg + s - 1, 1);
+    }
+    return t;
+}
+
+// Grab order of the speculative units u = k*R + q: list scheduling of W workers over
+// units with durations pb - pa and one predecessor each (in_k), highest remaining
+// chain (own + successors' rounds) first among the ready units.
+std::vector<int> spec_order(int64_t R, const std::vector<int4>& t, int64_t W) {
+    const int S = (int)t.size(), Sg = (S + 1) / 3;
+    std::vector<double> dur(S), prio(S);
+    for (int k = 0; k < S; ++k) dur[k] = t[k].y - t[k].x;
+    for (int s = 0; s < Sg; ++s) {
+        const double c = (s + 1 < Sg) ? dur[2 * Sg + s] : 0.0;     // C_{s+1} follows B_s
+        prio[Sg + s] = dur[Sg + s] + c;
+        prio[s] = dur[s] + prio[Sg + s];
+        if (s > 0) prio[2 * Sg + s - 1] = dur[2 * Sg + s - 1];
+    }
+    typedef std::pair<double, int64_t> Item;                      // (priority or time, unit)
+    std::priority_queue<Item> ready;
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> pending;
+    std::priority_queue<double, std::vector<double>, std::greater<double>> workers;
+    std::vector<std::vector<int>> succ(S);
+    for (int k = 0; k < S; ++k)
+        if (t[k].z >= 0) succ[t[k].z].push_back(k);
+    for (int64_t q = 0; q < R; ++q)
+        for (int k = 0; k < S; ++k)
+            if (t[k].z < 0) ready.push(Item(prio[k] - 1e-9 * (double)q, (int64_t)k * R + q));
+    for (int64_t w = 0; w < W; ++w) workers.push(0.0);
+    std::vector<int> order;
+    order.reserve((size_t)(R * S));
+    while ((int64_t)order.size() < R * S) {
+        double now = workers.top();
+        workers.pop();
+        auto release = [&](double upto) {
+            while (!pending.empty() && pending.top().first <= upto) {
+                const int64_t u = pending.top().second;
+                pending.pop();
+                ready.push(Item(prio[u / R] - 1e-9 * (double)(u % R), u));
+            }
+        };
+        release(now);
+        if (ready.empty()) {
+            now = pending.top().first;
+            release(now);
+        }
+        const int64_t u = ready.top().second;
+        ready.pop();
+        order.push_back((int)u);
+        const double fin = now + dur[u / R];
+        for (int k2 : succ[u / R]) pending.push(Item(fin, (int64_t)k2 * R + u % R));
+        workers.push(fin);
+    }
+    return order;
+}
+
+sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
                       int64_t* out_start, bool trace, BatchDev* dev_out = nullptr, Ragged rg = Ragged()) {
     if (N < 1 || Z < 0) return fail(SDTW_E_ARG, "N must be >= 1 and n_queries >= 0");
     if (Z > 0 && (!Q || !out_cost || !out_end || (trace && !out_start)))
@@ -493,23 +646,44 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.seg_done = nullptr;
     p.bnd_g = nullptr;
     p.cand = nullptr;
+    p.utab = nullptr;
+    int* fix_d = nullptr;
+    ctx->last_fixups = 0;
     if (cfg.persistent) {
         const size_t ent = cfg.half ? 2 : (trace ? 8 : 4) * (cfg.dual ? 2 : 1);
         const size_t R = (size_t)cfg.units;
-        const size_t done_b = ((sizeof(int) * R + 255) / 256) * 256;
-        const size_t nb = 256 + done_b + 16 * (size_t)Z * cfg.S + ent * R * cfg.Pd;
+        // done flags: per ring (sequential segments: a counter) or per unit (speculative)
+        const size_t done_b = ((sizeof(int) * R * (cfg.spec ? cfg.S : 1) + 255) / 256) * 256;
+        const size_t fix_b = cfg.spec ? ((sizeof(int) * R + 255) / 256) * 256 : 0;
+        const size_t bnd_units = cfg.spec ? R * cfg.S : R;
+        const size_t nb = 256 + done_b + fix_b + 16 * (size_t)Z * cfg.S + ent * bnd_units * cfg.Pd;
         s = grow(&ctx->ws_sched, &ctx->ws_sched_n, nb);
         if (s != SDTW_OK) return s;
         unsigned char* b = ctx->ws_sched;
         p.counter = reinterpret_cast<int*>(b);
         p.seg_done = reinterpret_cast<int*>(b + 256);
-        p.cand = b + 256 + done_b;
+        if (cfg.spec) fix_d = reinterpret_cast<int*>(b + 256 + done_b);
+        p.cand = b + 256 + done_b + fix_b;
         p.bnd_g = static_cast<unsigned char*>(p.cand) + 16 * (size_t)Z * cfg.S;
         CK(cudaMemsetAsync(b, 0, 256 + done_b, st));
-        if (rg.off || ctx->order_key[0] != (int64_t)R || ctx->order_key[1] != cfg.S ||
+        if (cfg.spec) {
+            const std::vector<int4> tab = spec_table(cfg.Pr, cfg.Sseg, cfg.Rc);
+            if (tab.size() > ctx->utab_n) {
+                if (ctx->utab_d) cudaFree(ctx->utab_d);
+                ctx->utab_d = nullptr;
+                ctx->utab_n = 0;
+                CK(cudaMalloc(&ctx->utab_d, tab.size() * sizeof(int4)));
+                ctx->utab_n = tab.size();
+            }
+            CK(cudaMemcpy(ctx->utab_d, tab.data(), tab.size() * sizeof(int4), cudaMemcpyHostToDevice));
+            p.utab = ctx->utab_d;
+        }
+        if (cfg.spec || rg.off || ctx->order_key[0] != (int64_t)R || ctx->order_key[1] != cfg.S ||
             ctx->order_key[2] != cfg.workers) {
             std::vector<int> ord;
-            if (rg.off) {
+            if (cfg.spec) {
+                ord = spec_order((int64_t)R, spec_table(cfg.Pr, cfg.Sseg, cfg.Rc), cfg.workers);
+            } else if (rg.off) {
                 std::vector<double> w(R);
                 for (int64_t q = 0; q < (int64_t)R; ++q)
                     w[q] = (double)std::max<int64_t>((*rg.off)[q + 1] - (*rg.off)[q], cfg.need);
@@ -525,7 +699,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
                 ctx->order_n = ord.size();
             }
             CK(cudaMemcpy(ctx->order_d, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice));
-            ctx->order_key[0] = rg.off ? -1 : (int64_t)R;             // ragged orders are not cached
+            ctx->order_key[0] = (rg.off || cfg.spec) ? -1 : (int64_t)R;   // ragged / speculative: not cached
             ctx->order_key[1] = cfg.S;
             ctx->order_key[2] = cfg.workers;
         }
@@ -534,7 +708,15 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     if (o.profile) CK(cudaEventRecord(ctx->ev0, st));
     s = launch_dp(cfg, o.fma != 0, trace, p, st);
     if (s != SDTW_OK) return s;
-    if (cfg.persistent) {
+    if (cfg.spec) {
+        sdtw::finalize_spec_kernel<<<(unsigned)Z, 128, 0, st>>>(
+            static_cast<const sdtw::Partial*>(p.cand), static_cast<const float*>(p.bnd_g), (int)Z, cfg.S, cfg.Sseg,
+            cfg.Pd, (int)N, ctx->flag_d, dc, de, fix_d);
+        CK(cudaGetLastError());
+        g_launches++;
+        s = spec_fixup(ctx, xd, Z, N, fix_d, dc, de, st);
+        if (s != SDTW_OK) return s;
+    } else if (cfg.persistent) {
         sdtw::finalize_kernel<<<(unsigned)((Z + 127) / 128), 128, 0, st>>>(
             static_cast<const sdtw::Partial*>(p.cand), (int)Z, cfg.S, ctx->flag_d, dc, de, trace ? ds : nullptr);
         CK(cudaGetLastError());
@@ -797,11 +979,12 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_CHUNK: if (v < 0 || v > 256) break; g_opt.chunk = (int)v; return SDTW_OK;
         case SDTW_OPT_PROFILE: if (v != 0 && v != 1) break; g_opt.profile = (int)v; return SDTW_OK;
         case SDTW_OPT_RING: if (v < 0 || v > 16384) break; g_opt.ring = (int)v; return SDTW_OK;
-        case SDTW_OPT_SCHED: if (v < 0 || v > 2) break; g_opt.sched = (int)v; return SDTW_OK;
+        case SDTW_OPT_SCHED: if (v < 0 || v > 3) break; g_opt.sched = (int)v; return SDTW_OK;
         case SDTW_OPT_SEGMENTS: if (v < 0 || v > 4096) break; g_opt.segments = (int)v; return SDTW_OK;
         case SDTW_OPT_WORKERS: if (v < 0 || v > 32) break; g_opt.workers = (int)v; return SDTW_OK;
         case SDTW_OPT_PRECISION: if (v != 16 && v != 32) break; g_opt.precision = (int)v; return SDTW_OK;
         case SDTW_OPT_PAD: if (v < 0 || v > (1 << 20)) break; g_opt.pad = (int)v; return SDTW_OK;
+        case SDTW_OPT_SPEC_ROUNDS: if (v < 0 || v > 4096) break; g_opt.spec_rounds = (int)v; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
     return fail(SDTW_E_ARG, "bad value for option " + std::to_string(key));
@@ -826,8 +1009,19 @@ sdtw_status sdtw_get_option(int key, int64_t* v) {
         case SDTW_OPT_WORKERS: *v = g_opt.workers; return SDTW_OK;
         case SDTW_OPT_PRECISION: *v = g_opt.precision; return SDTW_OK;
         case SDTW_OPT_PAD: *v = g_opt.pad; return SDTW_OK;
+        case SDTW_OPT_SPEC_ROUNDS: *v = g_opt.spec_rounds; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
+}
+
+sdtw_status sdtw_spec_recomputed(int64_t* n) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!n) return fail(SDTW_E_ARG, "NULL pointer");
+    Ctx* ctx;
+    sdtw_status s = get_ctx(&ctx);
+    if (s != SDTW_OK) return s;
+    *n = ctx->last_fixups;
+    return SDTW_OK;
 }
 
 sdtw_status sdtw_profile(double* dp_ms, int64_t* launches) {
@@ -860,6 +1054,8 @@ void sdtw_release(void) {
     cudaFree(c.ws_path);
     cudaFree(c.ws_rag);
     cudaFree(c.order_d);
+    cudaFree(c.utab_d);
+    cudaFree(c.ws_fix);
     cudaFree(c.flag_d);
     cudaFreeHost(c.flag_h);
     cudaEventDestroy(c.ev0);

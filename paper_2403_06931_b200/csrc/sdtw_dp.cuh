@@ -81,6 +81,12 @@ struct DpParams {
     int* seg_done;
     void* bnd_g;
     void* cand;
+    // speculative segments (utab != nullptr, cost/end only): unit kind k of a query is
+    // utab[k] = {pa, pb, in_k, db}: rounds [pa, pb), left boundary = the end column of
+    // kind in_k of the same query (-1: +inf), db != 0: no free start (virtual row -1 =
+    // +inf).  Every unit stores its end column at bnd_g[(q*S + k)*PdMax] and raises
+    // seg_done[q*S + k]; see run_batch_spec() in sdtw_api.cu.
+    const int4* utab;
 };
 
 template <bool TRACE> struct Entry { float d; };
@@ -519,17 +525,19 @@ __device__ __forceinline__ void stage_round(float* stage, const float* __restric
 
 // Round transition of chain c (slow path, rotation offset 0): new strip (y from
 // the staged copy), virtual row -1 = 0, and S(-1, j) = j+1 so that row 0 gets S = j.
+// (zrow = +inf instead of 0: no free start, the speculative correction units)
 template <int C, int WC, bool TRACE>
 __device__ __forceinline__ void enter_strip(RotRow<C, WC, TRACE>& row, Ys<C, WC>& Y, int c, long strip,
-                                            const float* ystage, LaneScalars<C>& ls, int off = 0) {
+                                            const float* ystage, LaneScalars<C>& ls, int off = 0,
+                                            float zrow = 0.0f) {
 #pragma unroll
     for (int w = 0; w < WC; ++w) Y.set(c, w, ystage[w]);
-    row.set_all(c, 0.0f, off);
+    row.set_all(c, zrow, off);
     if constexpr (TRACE) {
 #pragma unroll
         for (int k = 0; k < WC + 1; ++k) row.S[c][RotRow<C, WC, TRACE>::slot(k, off)] = (int)(strip * WC) + k + 1;
     }
-    ls.prevleft[c] = 0.0f;                 // D(-1, col0-1) = 0
+    ls.prevleft[c] = zrow;                 // D(-1, col0-1) = 0
     ls.prevleft_s[c] = (int)(strip * WC);
 }
 
@@ -652,7 +660,10 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     for (int unit_iter = 0;; ++unit_iter) {
     // ---- which unit: (query q, rounds [pa, pb))
     int q, seg = 0, pa = 0, pb = P.Pr;
-    if (P.persistent) {
+    int in_k = -1;                                          // speculative: source kind of the boundary
+    float zrow = 0.0f;                                      // virtual row -1 (+inf: no free start)
+    constexpr bool SPEC = !CLUSTER && !TRACE;               // speculative units: cost/end, one CTA
+    if (!CLUSTER && P.persistent) {
         if (threadIdx.x == 0) {
             const int raw = atomicAdd(P.counter, 1);
             *unit_sh = (P.order && raw < P.Z * P.S) ? P.order[raw] : raw;
@@ -663,11 +674,19 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         if (u >= P.Z * P.S) break;
         q = u % P.Z;
         seg = u / P.Z;
-        pa = (int)((long)seg * P.Pr / P.S);
-        pb = (int)((long)(seg + 1) * P.Pr / P.S);
-        if (seg > 0) {                                     // previous segment's boundary column
+        int wait_slot = -1, wait_val = 0;
+        if (SPEC && P.utab) {
+            const int4 d = P.utab[seg];
+            pa = d.x; pb = d.y; in_k = d.z; zrow = d.w ? INFINITY : 0.0f;
+            if (in_k >= 0) { wait_slot = q * P.S + in_k; wait_val = 1; }
+        } else {
+            pa = (int)((long)seg * P.Pr / P.S);
+            pb = (int)((long)(seg + 1) * P.Pr / P.S);
+            if (seg > 0) { wait_slot = q; wait_val = seg; }  // previous segment's boundary column
+        }
+        if (wait_slot >= 0) {
             long n = 0;                                    // (every thread polls: no split warps)
-            while (ld_acquire_gpu(P.seg_done + q) < seg) {
+            while (ld_acquire_gpu(P.seg_done + wait_slot) < wait_val) {
                 __nanosleep(256);
                 if (++n == (1LL << 26)) { printf("sdtw watchdog: unit %d waits segment\n", u); __trap(); }
             }
@@ -690,7 +709,9 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
 
     // ---- prologue: query rows -> smem, boundary ring (+inf, or the previous
     // segment's last column), counters
-    const E* bg = reinterpret_cast<const E*>(P.bnd_g) + (long)q * PdMax;
+    const bool spec = SPEC && P.utab;
+    const E* bg = reinterpret_cast<const E*>(P.bnd_g) + (spec ? ((long)q * P.S + max(in_k, 0)) : (long)q) * PdMax;
+    const bool bnd_in = spec ? in_k >= 0 : pa > 0;
     for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
         float* dst = XS ? xs + r : xs + (long)xrow_index(r, Pd, NC) * XC;
 #pragma unroll
@@ -700,7 +721,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
             dst[j] = (rr < N) ? xq[rr] : 0.0f;
         }
         E e;
-        if (pa > 0) {
+        if (bnd_in) {
             e = bg[r];
         } else {
             e.d = INFINITY;
@@ -793,7 +814,9 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         }
 #pragma unroll
         for (int c = 0; c < C; ++c)
-            if (rcs[c] == 0) enter_strip<C, WC, TRACE>(R, Y, c, (long)(pa + pcs[c]) * V + u0 + c, ylane + c * WC, ls, H);
+            if (rcs[c] == 0)
+                enter_strip<C, WC, TRACE>(R, Y, c, (long)(pa + pcs[c]) * V + u0 + c, ylane + c * WC, ls, H,
+                                          SPEC ? zrow : 0.0f);
         const XRow<C> x = load_xrow<C, XS>(xs, r0, Pd);
         row_cells<C, WC, FMA, TRACE, H>(R, Y, x, lin, lins, ls);
 #pragma unroll
@@ -1068,7 +1091,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                 if (better(pr.cost, pr.col, bc, bj)) { bc = pr.cost; bj = pr.col; bs = pr.start; }
             }
         }
-        if (P.persistent) {
+        if (!CLUSTER && P.persistent) {
             reinterpret_cast<Partial*>(P.cand)[(long)q * P.S + seg] = Partial{bc, bj, bs, 0};
         } else if (*P.err_flag == 0) {
             if (bj == 0x7fffffff) { bj = 0; bs = 0; }   // every cell overflowed (raw mode only)
@@ -1077,16 +1100,17 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
             if (TRACE && P.out_start) P.out_start[q] = bs;
         }
     }
-    if (P.persistent) {
+    if (!CLUSTER && P.persistent) {
         // hand this segment's last column to the next segment of the query
-        if (seg + 1 < P.S) {
-            E* bo = reinterpret_cast<E*>(P.bnd_g) + (long)q * PdMax;
+        if (spec || seg + 1 < P.S) {
+            E* bo = reinterpret_cast<E*>(P.bnd_g) + (spec ? (long)q * P.S + seg : (long)q) * PdMax;
             for (int r = threadIdx.x; r < Pd; r += blockDim.x) bo[r] = bnd[r];
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
-            st_release_gpu(P.seg_done + q, seg + 1);
+            if (spec) st_release_gpu(P.seg_done + q * P.S + seg, 1);
+            else st_release_gpu(P.seg_done + q, seg + 1);
         }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1109,6 +1133,46 @@ static __global__ void finalize_kernel(const Partial* __restrict__ cand, int Z, 
     out_cost[q] = b.cost;
     out_end[q] = b.col;
     if (out_start) out_start[q] = b.start;
+}
+
+// Speculative segments epilogue, one CTA per query.  Unit kinds:
+// A_s = k in [0, Sg) (first Rc rounds of segment s, +inf left boundary), B_s = Sg + s
+// (the rest of segment s), C_s = 2Sg + s - 1 for s >= 1 (A_s's rounds again, left
+// boundary = B_{s-1}'s end column, no free start).  The exact DP is the cell-wise min of
+// the free DP (A, B) and the boundary DP (C) -- the cell is monotone in its min input
+// and rounding is monotone -- and once the boundary DP is >= the free DP on a whole
+// column it stays so, so: result = lexmin over the A/B candidates and, per segment
+// whose C end column is >= the A end column on rows [0, N), its C candidate.  A
+// segment whose correction was not overtaken marks the query for recomputation
+// (fix[q] = 1); its result here is then discarded by the caller.
+static __global__ void finalize_spec_kernel(const Partial* __restrict__ cand, const float* __restrict__ bnd_g, int Z,
+                                            int S, int Sg, int PdMax, int N, const int* err_flag, float* out_cost,
+                                            int64_t* out_end, int* fix) {
+    const int q = blockIdx.x;
+    if (q >= Z || *err_flag) return;
+    const Partial* cq = cand + (long)q * S;
+    Partial b = cq[0];
+    for (int k = 1; k < 2 * Sg; ++k) {
+        const Partial c = cq[k];
+        if (better(c.cost, c.col, b.cost, b.col)) b = c;
+    }
+    int undominated = 0;
+    for (int s = 1; s < Sg; ++s) {
+        const float* a = bnd_g + ((long)q * S + s) * PdMax;
+        const float* c = bnd_g + ((long)q * S + 2 * Sg + s - 1) * PdMax;
+        int lt = 0;
+        for (int r = threadIdx.x; r < N; r += blockDim.x) lt |= c[r] < a[r];
+        lt = __syncthreads_or(lt);
+        if (lt) { undominated = 1; continue; }
+        const Partial cc = cq[2 * Sg + s - 1];
+        if (better(cc.cost, cc.col, b.cost, b.col)) b = cc;
+    }
+    if (threadIdx.x == 0) {
+        if (b.col == 0x7fffffff) b.col = 0;                  // every cell overflowed (raw mode only)
+        out_cost[q] = b.cost;
+        out_end[q] = b.col;
+        fix[q] = undominated;
+    }
 }
 
 }  // namespace sdtw

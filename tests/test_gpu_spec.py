@@ -1,0 +1,111 @@
+"""GPU parity of the speculative-segment schedule (SDTW_OPT_SCHED=3): every
+round-segment of a query starts at once from a +inf boundary, a correction pass of
+OPT_SPEC_ROUNDS rounds per segment boundary repairs the result, and queries whose
+correction is not overtaken in time are recomputed.  The result must be what the oracle
+gives (cost bit-exact, end exact or a tie) and bit-identical to the sequential schedules,
+both when the corrections succeed and when they are forced to fail."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2403_06931_b200 as sd  # noqa: E402
+from datagen import nanopore_queries, nanopore_reference  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def _inputs(Z, N, M, seed):
+    Y = oracle.znorm(nanopore_reference(M, seed)[None])[0]
+    Q = oracle.znorm(nanopore_queries(Z, N, M, seed))
+    return Q, Y
+
+
+def _run(Q, Y, **opts):
+    kw = dict(OPT_NORMALIZE=0)
+    kw.update(opts)
+    with sd.options(**kw):
+        sd.set_reference(torch.as_tensor(Y, device=DEV))
+        c, e = sd.batch(torch.as_tensor(np.ascontiguousarray(Q), device=DEV))
+        torch.cuda.synchronize()
+        fixed = sd.spec_recomputed()
+        launches = sd.profile()[1]
+    return c.cpu().numpy(), e.cpu().numpy(), fixed, launches
+
+
+def _check(Q, Y, c, e, fma=True, idx=None):
+    idx = np.arange(len(Q)) if idx is None else np.asarray(idx)
+    ref = oracle.sdtw(Q[idx], Y, fma=fma, last_rows=True)
+    assert np.array_equal(c[idx].view(np.uint32), ref["cost"].view(np.uint32)), (c[idx][:4], ref["cost"][:4])
+    for k in np.nonzero(e[idx] != ref["end"])[0]:
+        assert ref["last_rows"][k, e[idx][k]] == ref["cost"][k], (k, e[idx][k], ref["end"][k])
+
+
+@pytest.mark.parametrize("fma", [1, 0])
+def test_spec_small_bit_exact(fma):
+    Q, Y = _inputs(6, 300, 200_000, 61)
+    c, e, fixed, _ = _run(Q, Y, OPT_SCHED=3, OPT_FMA=fma)
+    _check(Q, Y, c, e, bool(fma))
+
+
+def test_spec_matches_sequential_schedules():
+    Q, Y = _inputs(20, 2000, 1_000_000, 62)
+    a = _run(Q, Y, OPT_SCHED=1)
+    b = _run(Q, Y, OPT_SCHED=3)
+    c = _run(Q, Y)                                  # auto: small batch -> speculative
+    for got in (b, c):
+        assert np.array_equal(got[0].view(np.uint32), a[0].view(np.uint32)) and np.array_equal(got[1], a[1])
+    assert c[3] == 3                                # normalise-check, DP, speculative finalize
+    _check(Q, Y, b[0], b[1], idx=[0, 7, 19])
+
+
+def test_spec_forced_recompute_is_exact():
+    """Queries that are exact copies of the reference across a segment boundary: the path
+    entering from the boundary scores ~0 for longer than a one-round correction (one-warp
+    rings: 960 columns per round), so the corrections fail and the queries are recomputed."""
+    M, N, Sg = 100_000, 1500, 8
+    Y = oracle.znorm(nanopore_reference(M, 63)[None])[0]
+    Pr = -(-M // 960)
+    bounds = [(s * Pr // Sg) * 960 for s in range(1, 6)]
+    Q = np.stack([Y[b - 200:b + N - 200] for b in bounds]).astype(np.float32)
+    c, e, fixed, _ = _run(Q, Y, OPT_SCHED=3, OPT_LANES=1, OPT_SPEC_ROUNDS=1, OPT_SEGMENTS=Sg)
+    assert fixed == len(bounds)
+    _check(Q, Y, c, e)
+    assert np.all(c == 0) and np.array_equal(e, np.array(bounds) + N - 201)
+
+
+def test_spec_short_corrections_mixed():
+    """Corrections of one round on a short query: most succeed; exact either way."""
+    Q, Y = _inputs(12, 120, 300_000, 64)
+    c, e, fixed, _ = _run(Q, Y, OPT_SCHED=3, OPT_SPEC_ROUNDS=1, OPT_SEGMENTS=20)
+    assert fixed < 12
+    _check(Q, Y, c, e)
+    a = _run(Q, Y, OPT_SCHED=1)
+    assert np.array_equal(c.view(np.uint32), a[0].view(np.uint32)) and np.array_equal(e, a[1])
+
+
+def test_spec_constant_signals_ties():
+    """All-zero inputs: every cell is 0, the boundary DP ties the free DP everywhere; the
+    end is the smallest column of the last row (N-1)."""
+    Y = np.zeros(150_000, np.float32)
+    Q = np.zeros((3, 200), np.float32)
+    c, e, fixed, _ = _run(Q, Y, OPT_SCHED=3)
+    assert np.all(c == 0) and np.all(e == 0) and fixed == 0
+
+
+def test_spec_errors():
+    Q, Y = _inputs(2, 50, 100_000, 65)
+    with sd.options(OPT_NORMALIZE=0, OPT_SCHED=3):
+        sd.set_reference(Y)
+        with pytest.raises(sd.SdtwError):
+            sd.traceback(Q)                          # cost / end only
+        bad = Q.copy()
+        bad[1, 3] = np.nan
+        with pytest.raises(sd.SdtwError) as ei:
+            sd.batch(bad)
+        assert ei.value.status == sd.E_NONFINITE
