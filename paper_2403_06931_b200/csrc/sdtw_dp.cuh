@@ -85,7 +85,7 @@ struct DpParams {
     // utab[k] = {pa, pb, in_k, db}: rounds [pa, pb), left boundary = the end column of
     // kind in_k of the same query (-1: +inf), db != 0: no free start (virtual row -1 =
     // +inf).  Every unit stores its end column at bnd_g[(q*S + k)*PdMax] and raises
-    // seg_done[q*S + k]; see run_batch_spec() in sdtw_api.cu.
+    // seg_done[q*S + k]; see spec_table() in sdtw_api.cu.
     const int4* utab;
 };
 
