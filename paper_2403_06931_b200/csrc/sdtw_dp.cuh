@@ -44,6 +44,9 @@
 #ifndef SDTW_C4_MINB
 #define SDTW_C4_MINB 3           // resident 4-warp CTAs per SM the 4-chain kernels are sized for
 #endif
+#ifndef SDTW_SPEC_CLUSTER
+#define SDTW_SPEC_CLUSTER 0   // 1: compile the (dead) speculative-unit decode into cluster kernels too
+#endif
 #ifndef SDTW_SPIN_NS
 #define SDTW_SPIN_NS 256         // nanosleep per flow-control poll (r01 A/B: 256 > 64 by 0.8 %)
 #endif
@@ -662,7 +665,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     int q, seg = 0, pa = 0, pb = P.Pr;
     int in_k = -1;                                          // speculative: source kind of the boundary
     float zrow = 0.0f;                                      // virtual row -1 (+inf: no free start)
-    constexpr bool SPEC = !CLUSTER && !TRACE;               // speculative units: cost/end, one CTA
+    constexpr bool SPEC = (!CLUSTER || SDTW_SPEC_CLUSTER) && !TRACE;   // speculative units: cost/end, one CTA
     if (!CLUSTER && P.persistent) {
         if (threadIdx.x == 0) {
             const int raw = atomicAdd(P.counter, 1);
