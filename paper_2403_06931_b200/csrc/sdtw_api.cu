@@ -189,7 +189,10 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
         return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) + " for this chain layout" +
                                     (C == 4 ? " (28)" : C == 2 ? " (14, 30)" : " (7, 15)"));
     const int64_t units = dual ? (Z + 1) / 2 : Z;
-    int GW = o.lanes > 0 ? o.lanes : 4;
+    // ragged batches with short reads: 8-warp rings (r01 c6 sweep, reads 500..8000 vs 1M:
+    // 4 warps 4.26, 6 4.96, 8 5.58 TCUPS; reads 500..2000: 5.20 -> 5.78; reads 2000..8000
+    // keep 4 warps: 6.87 vs 6.61)
+    int GW = o.lanes > 0 ? o.lanes : ((rg && rg->nmin < 2000 && !half && C == 2) ? 8 : 4);
     int CL = o.cluster > 0 ? o.cluster : 1;
     if (GW < 1 || GW > (dual ? 12 : (C == 4 ? 4 : 8)) || CL < 1 || CL > 16 || (dual && CL != 1))
         return fail(SDTW_E_ARG, "lanes / cluster out of range for this kernel");
