@@ -45,7 +45,8 @@
 #define SDTW_C4_MINB 3           // resident 4-warp CTAs per SM the 4-chain kernels are sized for
 #endif
 #ifndef SDTW_SPEC_CLUSTER
-#define SDTW_SPEC_CLUSTER 0   // 1: compile the (dead) speculative-unit decode into cluster kernels too
+#define SDTW_SPEC_CLUSTER 0   // debugging: 1 compiles the (dead) speculative-unit decode into cluster
+                              // kernels too, 2 also the (dead) persistent-unit code
 #endif
 #ifndef SDTW_SPIN_NS
 #define SDTW_SPIN_NS 256         // nanosleep per flow-control poll (r01 A/B: 256 > 64 by 0.8 %)
@@ -666,7 +667,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     int in_k = -1;                                          // speculative: source kind of the boundary
     float zrow = 0.0f;                                      // virtual row -1 (+inf: no free start)
     constexpr bool SPEC = (!CLUSTER || SDTW_SPEC_CLUSTER) && !TRACE;   // speculative units: cost/end, one CTA
-    if (!CLUSTER && P.persistent) {
+    if ((!CLUSTER || SDTW_SPEC_CLUSTER == 2) && P.persistent) {
         if (threadIdx.x == 0) {
             const int raw = atomicAdd(P.counter, 1);
             *unit_sh = (P.order && raw < P.Z * P.S) ? P.order[raw] : raw;
@@ -1094,7 +1095,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                 if (better(pr.cost, pr.col, bc, bj)) { bc = pr.cost; bj = pr.col; bs = pr.start; }
             }
         }
-        if (!CLUSTER && P.persistent) {
+        if ((!CLUSTER || SDTW_SPEC_CLUSTER == 2) && P.persistent) {
             reinterpret_cast<Partial*>(P.cand)[(long)q * P.S + seg] = Partial{bc, bj, bs, 0};
         } else if (*P.err_flag == 0) {
             if (bj == 0x7fffffff) { bj = 0; bs = 0; }   // every cell overflowed (raw mode only)
@@ -1103,7 +1104,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
             if (TRACE && P.out_start) P.out_start[q] = bs;
         }
     }
-    if (!CLUSTER && P.persistent) {
+    if ((!CLUSTER || SDTW_SPEC_CLUSTER == 2) && P.persistent) {
         // hand this segment's last column to the next segment of the query
         if (spec || seg + 1 < P.S) {
             E* bo = reinterpret_cast<E*>(P.bnd_g) + (spec ? (long)q * P.S + seg : (long)q) * PdMax;
