@@ -276,10 +276,10 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // correction pass of Rc rounds per segment boundary restores the exact result.
     const int64_t cols = V * WC;
     const int Rc = o.spec_rounds > 0 ? o.spec_rounds : (int)std::max<int64_t>(1, (3 * N + cols - 1) / cols);
-    const bool spec_ok = !trace && !half && !dual && CL == 1 && !rg && Pr >= 4 * (int64_t)(Rc + 1);
+    const bool spec_ok = !half && !dual && CL == 1 && !rg && Pr >= 4 * (int64_t)(Rc + 1);
     if (sched == 3 && !spec_ok)
-        return fail(SDTW_E_ARG, "speculative segments need cost/end, fp32, no clusters, fixed-length "
-                                "queries and >= 4 segments of more than OPT_SPEC_ROUNDS rounds");
+        return fail(SDTW_E_ARG, "speculative segments need fp32, no clusters, fixed-length queries "
+                                "and >= 4 segments of more than OPT_SPEC_ROUNDS rounds");
     int occ = 0;
     if (sched == 3 || (sched == 0 && spec_ok)) {
         DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false, dual, half, xs);
@@ -440,7 +440,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
 // (fix[q] != 0) are recomputed with sequential segments from their normalised rows and
 // their results replace the speculative ones.
 sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const int* fix_d, float* dc, int64_t* de,
-                       cudaStream_t st) {
+                       int64_t* ds, cudaStream_t st) {
     std::vector<int> fix((size_t)Z);
     CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(fix.data(), fix_d, (size_t)Z * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -451,11 +451,12 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const in
         if (fix[q]) idx.push_back(q);
     if (idx.empty()) return SDTW_OK;
     const int64_t F = (int64_t)idx.size();
-    const size_t need = 3 * (size_t)F + (size_t)F * (size_t)N;   // (end, cost) per query + rows
+    const size_t need = 5 * (size_t)F + (size_t)F * (size_t)N;   // (end, start, cost) per query + rows
     sdtw_status s = grow(&ctx->ws_fix, &ctx->ws_fix_n, need);
     if (s != SDTW_OK) return s;
     int64_t* fe = reinterpret_cast<int64_t*>(ctx->ws_fix);
-    float* fc = ctx->ws_fix + 2 * F;
+    int64_t* fs = fe + F;
+    float* fc = ctx->ws_fix + 4 * F;
     float* rows = fc + F;
     for (int64_t k = 0; k < F; ++k)
         CK(cudaMemcpyAsync(rows + k * N, xd + idx[k] * N, (size_t)N * sizeof(float), cudaMemcpyDeviceToDevice, st));
@@ -465,12 +466,13 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const in
     g_opt.sched = 1;                                  // one CTA per ring: no speculation again
     g_opt.stream = st;
     const int64_t fixed_before = F;
-    s = run_batch(rows, F, N, fc, fe, nullptr, false, nullptr, Ragged());
+    s = run_batch(rows, F, N, fc, fe, ds ? fs : nullptr, ds != nullptr, nullptr, Ragged());
     g_opt = saved;
     if (s != SDTW_OK) return s;
     for (int64_t k = 0; k < F; ++k) {
         CK(cudaMemcpyAsync(dc + idx[k], fc + k, sizeof(float), cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(de + idx[k], fe + k, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+        if (ds) CK(cudaMemcpyAsync(ds + idx[k], fs + k, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     }
     ctx->last_fixups = fixed_before;
     return SDTW_OK;
@@ -714,10 +716,10 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     if (cfg.spec) {
         sdtw::finalize_spec_kernel<<<(unsigned)Z, 128, 0, st>>>(
             static_cast<const sdtw::Partial*>(p.cand), static_cast<const float*>(p.bnd_g), (int)Z, cfg.S, cfg.Sseg,
-            cfg.Pd, (int)N, ctx->flag_d, dc, de, fix_d);
+            cfg.Pd, (int)N, ctx->flag_d, dc, de, trace ? ds : nullptr, fix_d);
         CK(cudaGetLastError());
         g_launches++;
-        s = spec_fixup(ctx, xd, Z, N, fix_d, dc, de, st);
+        s = spec_fixup(ctx, xd, Z, N, fix_d, dc, de, trace ? ds : nullptr, st);
         if (s != SDTW_OK) return s;
     } else if (cfg.persistent) {
         sdtw::finalize_kernel<<<(unsigned)((Z + 127) / 128), 128, 0, st>>>(

@@ -85,7 +85,7 @@ struct DpParams {
     int* seg_done;
     void* bnd_g;
     void* cand;
-    // speculative segments (utab != nullptr, cost/end only): unit kind k of a query is
+    // speculative segments (utab != nullptr): unit kind k of a query is
     // utab[k] = {pa, pb, in_k, db}: rounds [pa, pb), left boundary = the end column of
     // kind in_k of the same query (-1: +inf), db != 0: no free start (virtual row -1 =
     // +inf).  Every unit stores its end column at bnd_g[(q*S + k)*PdMax] and raises
@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     int q, seg = 0, pa = 0, pb = P.Pr;
     int in_k = -1;                                          // speculative: source kind of the boundary
     float zrow = 0.0f;                                      // virtual row -1 (+inf: no free start)
-    constexpr bool SPEC = (!CLUSTER || SDTW_SPEC_CLUSTER) && !TRACE;   // speculative units: cost/end, one CTA
+    constexpr bool SPEC = !CLUSTER || SDTW_SPEC_CLUSTER;    // speculative units: one CTA per ring
     if ((!CLUSTER || SDTW_SPEC_CLUSTER == 2) && P.persistent) {
         if (threadIdx.x == 0) {
             const int raw = atomicAdd(P.counter, 1);
@@ -1146,35 +1146,47 @@ static __global__ void finalize_kernel(const Partial* __restrict__ cand, int Z, 
 // the free DP (A, B) and the boundary DP (C) -- the cell is monotone in its min input
 // and rounding is monotone -- and once the boundary DP is >= the free DP on a whole
 // column it stays so, so: result = lexmin over the A/B candidates and, per segment
-// whose C end column is >= the A end column on rows [0, N), its C candidate.  A
-// segment whose correction was not overtaken marks the query for recomputation
-// (fix[q] = 1); its result here is then discarded by the caller.
+// whose C end column is >= the A end column on rows [0, N) ("overtaken"), its C
+// candidate.  With start columns (stride 2: {d, s} entries) the check is strict (C > A,
+// or both +inf) and an exact (cost, col) tie between the best A/B and the best C
+// candidate is ambiguous too: on strictly-won cells the winner's start is the true one,
+// on ties the priority rule of the merged DP decides.  A query with a
+// segment not overtaken (or such a tie) is marked for recomputation (fix[q] = 1).
 static __global__ void finalize_spec_kernel(const Partial* __restrict__ cand, const float* __restrict__ bnd_g, int Z,
                                             int S, int Sg, int PdMax, int N, const int* err_flag, float* out_cost,
-                                            int64_t* out_end, int* fix) {
+                                            int64_t* out_end, int64_t* out_start, int* fix) {
     const int q = blockIdx.x;
     if (q >= Z || *err_flag) return;
+    const bool trace = out_start != nullptr;
+    const int es = trace ? 2 : 1;                          // floats per boundary entry
     const Partial* cq = cand + (long)q * S;
     Partial b = cq[0];
     for (int k = 1; k < 2 * Sg; ++k) {
         const Partial c = cq[k];
         if (better(c.cost, c.col, b.cost, b.col)) b = c;
     }
+    Partial bc{INFINITY, 0x7fffffff, 0, 0};                // best correction candidate
     int undominated = 0;
     for (int s = 1; s < Sg; ++s) {
-        const float* a = bnd_g + ((long)q * S + s) * PdMax;
-        const float* c = bnd_g + ((long)q * S + 2 * Sg + s - 1) * PdMax;
+        const float* a = bnd_g + ((long)q * S + s) * PdMax * es;
+        const float* c = bnd_g + ((long)q * S + 2 * Sg + s - 1) * PdMax * es;
         int lt = 0;
-        for (int r = threadIdx.x; r < N; r += blockDim.x) lt |= c[r] < a[r];
+        for (int r = threadIdx.x; r < N; r += blockDim.x) {
+            const float av = a[(long)r * es], cv = c[(long)r * es];
+            lt |= trace ? !(cv > av || (cv == INFINITY && av == INFINITY)) : cv < av;
+        }
         lt = __syncthreads_or(lt);
         if (lt) { undominated = 1; continue; }
         const Partial cc = cq[2 * Sg + s - 1];
-        if (better(cc.cost, cc.col, b.cost, b.col)) b = cc;
+        if (better(cc.cost, cc.col, bc.cost, bc.col)) bc = cc;
     }
     if (threadIdx.x == 0) {
-        if (b.col == 0x7fffffff) b.col = 0;                  // every cell overflowed (raw mode only)
+        if (trace && bc.cost == b.cost && bc.col == b.col && b.col != 0x7fffffff) undominated = 1;
+        if (better(bc.cost, bc.col, b.cost, b.col)) b = bc;
+        if (b.col == 0x7fffffff) { b.col = 0; b.start = 0; }   // every cell overflowed (raw mode only)
         out_cost[q] = b.cost;
         out_end[q] = b.col;
+        if (trace) out_start[q] = b.start;
         fix[q] = undominated;
     }
 }

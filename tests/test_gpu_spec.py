@@ -3,7 +3,8 @@ round-segment of a query starts at once from a +inf boundary, a correction pass 
 OPT_SPEC_ROUNDS rounds per segment boundary repairs the result, and queries whose
 correction is not overtaken in time are recomputed.  The result must be what the oracle
 gives (cost bit-exact, end exact or a tie) and bit-identical to the sequential schedules,
-both when the corrections succeed and when they are forced to fail."""
+both when the corrections succeed and when they are forced to fail, for cost / end and for
+the start index."""
 import numpy as np
 import pytest
 
@@ -26,24 +27,31 @@ def _inputs(Z, N, M, seed):
     return Q, Y
 
 
-def _run(Q, Y, **opts):
+def _run(Q, Y, start=False, **opts):
     kw = dict(OPT_NORMALIZE=0)
     kw.update(opts)
     with sd.options(**kw):
         sd.set_reference(torch.as_tensor(Y, device=DEV))
-        c, e = sd.batch(torch.as_tensor(np.ascontiguousarray(Q), device=DEV))
+        Qt = torch.as_tensor(np.ascontiguousarray(Q), device=DEV)
+        out = sd.traceback(Qt) if start else sd.batch(Qt)
         torch.cuda.synchronize()
         fixed = sd.spec_recomputed()
         launches = sd.profile()[1]
-    return c.cpu().numpy(), e.cpu().numpy(), fixed, launches
+    out = [o.cpu().numpy() for o in out]
+    if start:
+        return out[0], out[1], fixed, launches, out[2]
+    return out[0], out[1], fixed, launches
 
 
-def _check(Q, Y, c, e, fma=True, idx=None):
+def _check(Q, Y, c, e, fma=True, idx=None, s=None):
     idx = np.arange(len(Q)) if idx is None else np.asarray(idx)
-    ref = oracle.sdtw(Q[idx], Y, fma=fma, last_rows=True)
+    ref = oracle.sdtw(Q[idx], Y, fma=fma, last_rows=True, start=s is not None)
     assert np.array_equal(c[idx].view(np.uint32), ref["cost"].view(np.uint32)), (c[idx][:4], ref["cost"][:4])
     for k in np.nonzero(e[idx] != ref["end"])[0]:
         assert ref["last_rows"][k, e[idx][k]] == ref["cost"][k], (k, e[idx][k], ref["end"][k])
+    if s is not None:
+        same = e[idx] == ref["end"]
+        assert np.array_equal(s[idx][same], ref["start"][same]), (s[idx][:4], ref["start"][:4])
 
 
 @pytest.mark.parametrize("fma", [1, 0])
@@ -51,6 +59,28 @@ def test_spec_small_bit_exact(fma):
     Q, Y = _inputs(6, 300, 200_000, 61)
     c, e, fixed, _ = _run(Q, Y, OPT_SCHED=3, OPT_FMA=fma)
     _check(Q, Y, c, e, bool(fma))
+
+
+@pytest.mark.parametrize("fma", [1, 0])
+def test_spec_start_index_bit_exact(fma):
+    Q, Y = _inputs(6, 300, 200_000, 66)
+    c, e, fixed, _, s = _run(Q, Y, start=True, OPT_SCHED=3, OPT_FMA=fma)
+    _check(Q, Y, c, e, bool(fma), s=s)
+    a = _run(Q, Y, start=True, OPT_SCHED=1, OPT_FMA=fma)
+    assert np.array_equal(c.view(np.uint32), a[0].view(np.uint32))
+    assert np.array_equal(e, a[1]) and np.array_equal(s, a[4])
+
+
+def test_spec_start_index_embedded_matches():
+    """Exact embeddings (cost 0, known start / end) spread over the reference, some across
+    segment boundaries: start columns exact."""
+    M, N = 300_000, 400
+    Y = oracle.znorm(nanopore_reference(M, 67)[None])[0]
+    rng = np.random.default_rng(67)
+    starts = np.sort(rng.integers(0, M - N, 10))
+    Q = np.stack([Y[a:a + N] for a in starts]).astype(np.float32)
+    c, e, fixed, _, s = _run(Q, Y, start=True, OPT_SCHED=3, OPT_SEGMENTS=20)
+    assert np.all(c == 0) and np.array_equal(s, starts) and np.array_equal(e, starts + N - 1)
 
 
 def test_spec_matches_sequential_schedules():
@@ -77,6 +107,8 @@ def test_spec_forced_recompute_is_exact():
     assert fixed == len(bounds)
     _check(Q, Y, c, e)
     assert np.all(c == 0) and np.array_equal(e, np.array(bounds) + N - 201)
+    c, e, fixed, _, st = _run(Q, Y, start=True, OPT_SCHED=3, OPT_LANES=1, OPT_SPEC_ROUNDS=1, OPT_SEGMENTS=Sg)
+    assert fixed == len(bounds) and np.all(c == 0) and np.array_equal(st, np.array(bounds) - 200)
 
 
 def test_spec_short_corrections_mixed():
@@ -96,14 +128,18 @@ def test_spec_constant_signals_ties():
     Q = np.zeros((3, 200), np.float32)
     c, e, fixed, _ = _run(Q, Y, OPT_SCHED=3)
     assert np.all(c == 0) and np.all(e == 0) and fixed == 0
+    # start index: the tie between boundary and free paths is not a strict win -> recompute
+    c, e, fixed, _, s = _run(Q, Y, start=True, OPT_SCHED=3)
+    assert np.all(c == 0) and np.all(e == 0) and np.all(s == 0) and fixed == 3
 
 
 def test_spec_errors():
     Q, Y = _inputs(2, 50, 100_000, 65)
     with sd.options(OPT_NORMALIZE=0, OPT_SCHED=3):
         sd.set_reference(Y)
-        with pytest.raises(sd.SdtwError):
-            sd.traceback(Q)                          # cost / end only
+        with sd.options(OPT_CLUSTER=2):
+            with pytest.raises(sd.SdtwError):
+                sd.batch(Q)                          # one CTA per ring only
         bad = Q.copy()
         bad[1, 3] = np.nan
         with pytest.raises(sd.SdtwError) as ei:
