@@ -289,15 +289,19 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
             return fail(SDTW_E_CUDA, "occupancy query failed");
         }
     }
-    // auto: when the rings cannot fill every resident CTA slot (r01 C3 sweep, 10M x 2000:
-    // Z=64 1.88 -> 7.91 TCUPS, Z=200 4.24 -> 7.65, Z=300 7.16 -> 7.67, Z=444 8.46 = 8.48)
-    if (sched == 3 || (sched == 0 && spec_ok && units < (int64_t)occ * ctx.sms)) {
+    // auto whenever it applies (r01 sweeps, 10M x 2000, TCUPS sequential -> speculative:
+    // Z=64 1.88 -> 8.15, Z=200 4.24 -> 8.54, Z=512 (config 3) 8.40 -> 8.78; 1M x 2000:
+    // 8.13 -> 8.13; 100K: 7.05 -> 7.05; start index Z=512 equal): every SM runs all its
+    // resident CTA slots (4 here, vs 3 rings' worth of chains) and no unit waits for a
+    // long predecessor segment.
+    if (sched == 3 || (sched == 0 && spec_ok)) {
         const int per_sm = o.workers > 0 ? std::min(o.workers, occ) : occ;
         const int64_t W = (int64_t)per_sm * ctx.sms;
-        // segments: about four units per worker (Z=64: 7 segments 6.21, 14 7.68, 28 7.91,
-        // 56 7.99 TCUPS), each > Rc rounds and long enough that the correction passes stay
-        // a small share (Rc / segment length)
-        int64_t Sg = o.segments > 0 ? o.segments : (4 * W + units - 1) / units;
+        // segments: about five long (B) units per worker (Z=512: 5 segments 8.40, 6 8.78,
+        // 8 8.74, 12 8.65; Z=64: 28 7.91, 40 8.15, 65 8.02; Z=200: 10 8.32, 16 8.54, 24 8.48),
+        // each > Rc rounds and long enough that the correction passes stay a small share
+        // (Rc / segment length)
+        int64_t Sg = o.segments > 0 ? o.segments : (10 * W + units) / (2 * units);
         Sg = std::min<int64_t>(Sg, Pr / std::max<int64_t>(4 * (Rc + 1), 8));
         Sg = std::max<int64_t>(Sg, 2);
         if (Pr / Sg <= Rc) return fail(SDTW_E_ARG, "speculative segments shorter than the correction pass");
