@@ -64,8 +64,8 @@ enum {
                                3 speculative segments: every round-segment of a query starts
                                at once from a +inf boundary, then a short correction pass per
                                segment boundary repairs the result exactly (also the start
-                               index; fp32, no clusters, fixed-length batches; auto when the
-                               rings cannot fill every resident CTA slot) */
+                               index; fp32, no clusters, fixed-length batches; the auto
+                               choice for those) */
     SDTW_OPT_SEGMENTS = 12, /* round segments per query under persistent scheduling; 0 = auto */
     SDTW_OPT_WORKERS = 13,  /* resident CTAs per SM under persistent scheduling; 0 = auto
                                (min(occupancy, n_queries / #SMs)) */
