@@ -276,10 +276,10 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // correction pass of Rc rounds per segment boundary restores the exact result.
     const int64_t cols = V * WC;
     const int Rc = o.spec_rounds > 0 ? o.spec_rounds : (int)std::max<int64_t>(1, (3 * N + cols - 1) / cols);
-    const bool spec_ok = !half && !dual && CL == 1 && !rg && Pr >= 4 * (int64_t)(Rc + 1);
+    const bool spec_ok = !half && !dual && CL == 1 && Pr >= 4 * (int64_t)(Rc + 1);
     if (sched == 3 && !spec_ok)
-        return fail(SDTW_E_ARG, "speculative segments need fp32, no clusters, fixed-length queries "
-                                "and >= 4 segments of more than OPT_SPEC_ROUNDS rounds");
+        return fail(SDTW_E_ARG, "speculative segments need fp32, no clusters and >= 4 segments of "
+                                "more than OPT_SPEC_ROUNDS rounds");
     int occ = 0;
     if (sched == 3 || (sched == 0 && spec_ok)) {
         DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false, dual, half, xs);
@@ -301,6 +301,8 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
         // 8 8.74, 12 8.65; Z=64: 28 7.91, 40 8.15, 65 8.02; Z=200: 10 8.32, 16 8.54, 24 8.48),
         // each > Rc rounds and long enough that the correction passes stay a small share
         // (Rc / segment length)
+        // (ragged batches, with the round-period-weighted grab order: c6 sweep 3 segments
+        // 7.40, 4 7.14, 5 6.90, 8 6.67 TCUPS; sequential segments 5.63)
         int64_t Sg = o.segments > 0 ? o.segments : (10 * W + units) / (2 * units);
         Sg = std::min<int64_t>(Sg, Pr / std::max<int64_t>(4 * (Rc + 1), 8));
         Sg = std::max<int64_t>(Sg, 2);
@@ -443,8 +445,8 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
 // Speculative segments: queries whose correction pass was not overtaken within Rc rounds
 // (fix[q] != 0) are recomputed with sequential segments from their normalised rows and
 // their results replace the speculative ones.
-sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const int* fix_d, float* dc, int64_t* de,
-                       int64_t* ds, cudaStream_t st) {
+sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const std::vector<int64_t>* off,
+                       const int* fix_d, float* dc, int64_t* de, int64_t* ds, cudaStream_t st) {
     std::vector<int> fix((size_t)Z);
     CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(fix.data(), fix_d, (size_t)Z * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -455,22 +457,39 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const in
         if (fix[q]) idx.push_back(q);
     if (idx.empty()) return SDTW_OK;
     const int64_t F = (int64_t)idx.size();
-    const size_t need = 5 * (size_t)F + (size_t)F * (size_t)N;   // (end, start, cost) per query + rows
+    // the recomputed queries' rows, packed (ragged batches: with their own offsets)
+    std::vector<int64_t> off2((size_t)F + 1, 0);
+    int64_t nmin2 = INT64_MAX, nmax2 = 0;
+    for (int64_t k = 0; k < F; ++k) {
+        const int64_t n = off ? (*off)[idx[k] + 1] - (*off)[idx[k]] : N;
+        off2[k + 1] = off2[k] + n;
+        nmin2 = std::min(nmin2, n);
+        nmax2 = std::max(nmax2, n);
+    }
+    const size_t need = 5 * (size_t)F + (size_t)off2[F];           // (end, start, cost) per query + rows
     sdtw_status s = grow(&ctx->ws_fix, &ctx->ws_fix_n, need);
     if (s != SDTW_OK) return s;
     int64_t* fe = reinterpret_cast<int64_t*>(ctx->ws_fix);
     int64_t* fs = fe + F;
     float* fc = ctx->ws_fix + 4 * F;
     float* rows = fc + F;
-    for (int64_t k = 0; k < F; ++k)
-        CK(cudaMemcpyAsync(rows + k * N, xd + idx[k] * N, (size_t)N * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    for (int64_t k = 0; k < F; ++k) {
+        const int64_t src = off ? (*off)[idx[k]] : idx[k] * N;
+        CK(cudaMemcpyAsync(rows + off2[k], xd + src, (size_t)(off2[k + 1] - off2[k]) * sizeof(float),
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    Ragged rg2;
+    if (off) {
+        rg2.off = &off2;
+        rg2.nmin = nmin2;
+    }
     const Options saved = g_opt;
     g_opt.normalize = 0;
     g_opt.profile = 0;
     g_opt.sched = 1;                                  // one CTA per ring: no speculation again
     g_opt.stream = st;
     const int64_t fixed_before = F;
-    s = run_batch(rows, F, N, fc, fe, ds ? fs : nullptr, ds != nullptr, nullptr, Ragged());
+    s = run_batch(rows, F, off ? nmax2 : N, fc, fe, ds ? fs : nullptr, ds != nullptr, nullptr, rg2);
     g_opt = saved;
     if (s != SDTW_OK) return s;
     for (int64_t k = 0; k < F; ++k) {
@@ -500,7 +519,9 @@ std::vector<int4> spec_table(int Pr, int Sg, int Rc) {
 // Grab order of the speculative units u = k*R + q: list scheduling of W workers over
 // units with durations pb - pa and one predecessor each (in_k), highest remaining
 // chain (own + successors' rounds) first among the ready units.
-std::vector<int> spec_order(int64_t R, const std::vector<int4>& t, int64_t W) {
+std::vector<int> spec_order(int64_t R, const std::vector<int4>& t, int64_t W, const std::vector<double>* wq = nullptr) {
+    // wq: per-ring weight (ragged batches: round period of the query), 1 otherwise
+    auto wt = [&](int64_t q) { return wq ? (*wq)[q] : 1.0; };
     const int S = (int)t.size(), Sg = (S + 1) / 3;
     std::vector<double> dur(S), prio(S);
     for (int k = 0; k < S; ++k) dur[k] = t[k].y - t[k].x;
@@ -519,7 +540,7 @@ std::vector<int> spec_order(int64_t R, const std::vector<int4>& t, int64_t W) {
         if (t[k].z >= 0) succ[t[k].z].push_back(k);
     for (int64_t q = 0; q < R; ++q)
         for (int k = 0; k < S; ++k)
-            if (t[k].z < 0) ready.push(Item(prio[k] - 1e-9 * (double)q, (int64_t)k * R + q));
+            if (t[k].z < 0) ready.push(Item(prio[k] * wt(q) - 1e-9 * (double)q, (int64_t)k * R + q));
     for (int64_t w = 0; w < W; ++w) workers.push(0.0);
     std::vector<int> order;
     order.reserve((size_t)(R * S));
@@ -530,7 +551,7 @@ std::vector<int> spec_order(int64_t R, const std::vector<int4>& t, int64_t W) {
             while (!pending.empty() && pending.top().first <= upto) {
                 const int64_t u = pending.top().second;
                 pending.pop();
-                ready.push(Item(prio[u / R] - 1e-9 * (double)(u % R), u));
+                ready.push(Item(prio[u / R] * wt(u % R) - 1e-9 * (double)(u % R), u));
             }
         };
         release(now);
@@ -541,7 +562,7 @@ std::vector<int> spec_order(int64_t R, const std::vector<int4>& t, int64_t W) {
         const int64_t u = ready.top().second;
         ready.pop();
         order.push_back((int)u);
-        const double fin = now + dur[u / R];
+        const double fin = now + dur[u / R] * wt(u % R);
         for (int k2 : succ[u / R]) pending.push(Item(fin, (int64_t)k2 * R + u % R));
         workers.push(fin);
     }
@@ -691,7 +712,13 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
             ctx->order_key[2] != cfg.workers) {
             std::vector<int> ord;
             if (cfg.spec) {
-                ord = spec_order((int64_t)R, spec_table(cfg.Pr, cfg.Sseg, cfg.Rc), cfg.workers);
+                std::vector<double> w;
+                if (rg.off) {
+                    w.resize(R);
+                    for (int64_t q = 0; q < (int64_t)R; ++q)
+                        w[q] = (double)std::max<int64_t>((*rg.off)[q + 1] - (*rg.off)[q], cfg.need);
+                }
+                ord = spec_order((int64_t)R, spec_table(cfg.Pr, cfg.Sseg, cfg.Rc), cfg.workers, rg.off ? &w : nullptr);
             } else if (rg.off) {
                 std::vector<double> w(R);
                 for (int64_t q = 0; q < (int64_t)R; ++q)
@@ -720,10 +747,10 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     if (cfg.spec) {
         sdtw::finalize_spec_kernel<<<(unsigned)Z, 128, 0, st>>>(
             static_cast<const sdtw::Partial*>(p.cand), static_cast<const float*>(p.bnd_g), (int)Z, cfg.S, cfg.Sseg,
-            cfg.Pd, (int)N, ctx->flag_d, dc, de, trace ? ds : nullptr, fix_d);
+            cfg.Pd, (int)N, qlen_d, ctx->flag_d, dc, de, trace ? ds : nullptr, fix_d);
         CK(cudaGetLastError());
         g_launches++;
-        s = spec_fixup(ctx, xd, Z, N, fix_d, dc, de, trace ? ds : nullptr, st);
+        s = spec_fixup(ctx, xd, Z, N, rg.off, fix_d, dc, de, trace ? ds : nullptr, st);
         if (s != SDTW_OK) return s;
     } else if (cfg.persistent) {
         sdtw::finalize_kernel<<<(unsigned)((Z + 127) / 128), 128, 0, st>>>(

@@ -1153,10 +1153,11 @@ static __global__ void finalize_kernel(const Partial* __restrict__ cand, int Z, 
 // on ties the priority rule of the merged DP decides.  A query with a
 // segment not overtaken (or such a tie) is marked for recomputation (fix[q] = 1).
 static __global__ void finalize_spec_kernel(const Partial* __restrict__ cand, const float* __restrict__ bnd_g, int Z,
-                                            int S, int Sg, int PdMax, int N, const int* err_flag, float* out_cost,
-                                            int64_t* out_end, int64_t* out_start, int* fix) {
+                                            int S, int Sg, int PdMax, int N, const int* qlen, const int* err_flag,
+                                            float* out_cost, int64_t* out_end, int64_t* out_start, int* fix) {
     const int q = blockIdx.x;
     if (q >= Z || *err_flag) return;
+    if (qlen) N = qlen[q];                                 // ragged batch: this query's rows
     const bool trace = out_start != nullptr;
     const int es = trace ? 2 : 1;                          // floats per boundary entry
     const Partial* cq = cand + (long)q * S;

@@ -111,6 +111,33 @@ def test_spec_forced_recompute_is_exact():
     assert fixed == len(bounds) and np.all(c == 0) and np.array_equal(st, np.array(bounds) - 200)
 
 
+def test_spec_ragged_forced_recompute_is_exact():
+    """Ragged batch: reads copying the reference across segment boundaries (recomputed through
+    a ragged sub-batch) next to random reads (not recomputed); every result exact."""
+    M, Sg = 100_000, 8
+    Y = oracle.znorm(nanopore_reference(M, 68)[None])[0]
+    Pr = -(-M // 960)
+    bounds = [(s * Pr // Sg) * 960 for s in (1, 3, 5)]
+    lens = [1500, 1300, 1700]
+    qs = [Y[b - 200:b - 200 + n].astype(np.float32) for b, n in zip(bounds, lens)]
+    qs += [oracle.znorm(nanopore_queries(1, n, M, 680 + n))[0] for n in (90, 400, 1100)]
+    off = np.zeros(len(qs) + 1, np.int64)
+    off[1:] = np.cumsum([len(q) for q in qs])
+    with sd.options(OPT_NORMALIZE=0, OPT_SCHED=3, OPT_LANES=1, OPT_SPEC_ROUNDS=1, OPT_SEGMENTS=Sg):
+        sd.set_reference(Y)
+        c, e, st = sd.batch_ragged(np.concatenate(qs), off, start=True)
+        fixed = sd.spec_recomputed()
+    assert fixed >= 3
+    for k, q in enumerate(qs):
+        r = oracle.sdtw(q[None], Y, start=True, last_rows=True)
+        assert c[k] == r["cost"][0], k
+        if e[k] != r["end"][0]:
+            assert r["last_rows"][0, e[k]] == r["cost"][0], k
+        else:
+            assert st[k] == r["start"][0], k
+    assert np.all(c[:3] == 0) and np.array_equal(st[:3], np.array(bounds) - 200)
+
+
 def test_spec_short_corrections_mixed():
     """Corrections of one round on a short query: most succeed; exact either way."""
     Q, Y = _inputs(12, 120, 300_000, 64)
