@@ -276,10 +276,10 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // correction pass of Rc rounds per segment boundary restores the exact result.
     const int64_t cols = V * WC;
     const int Rc = o.spec_rounds > 0 ? o.spec_rounds : (int)std::max<int64_t>(1, (3 * N + cols - 1) / cols);
-    const bool spec_ok = !half && !dual && CL == 1 && Pr >= 4 * (int64_t)(Rc + 1);
+    const bool spec_ok = !dual && CL == 1 && Pr >= 4 * (int64_t)(Rc + 1);
     if (sched == 3 && !spec_ok)
-        return fail(SDTW_E_ARG, "speculative segments need fp32, no clusters and >= 4 segments of "
-                                "more than OPT_SPEC_ROUNDS rounds");
+        return fail(SDTW_E_ARG, "speculative segments need no clusters, OPT_PACKED <= 2 and >= 4 "
+                                "segments of more than OPT_SPEC_ROUNDS rounds");
     int occ = 0;
     if (sched == 3 || (sched == 0 && spec_ok)) {
         DpKernel k = pick_kernel(C, WC, o.fma != 0, trace, false, dual, half, xs);
@@ -746,8 +746,8 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     if (s != SDTW_OK) return s;
     if (cfg.spec) {
         sdtw::finalize_spec_kernel<<<(unsigned)Z, 128, 0, st>>>(
-            static_cast<const sdtw::Partial*>(p.cand), static_cast<const float*>(p.bnd_g), (int)Z, cfg.S, cfg.Sseg,
-            cfg.Pd, (int)N, qlen_d, ctx->flag_d, dc, de, trace ? ds : nullptr, fix_d);
+            static_cast<const sdtw::Partial*>(p.cand), p.bnd_g, (int)Z, cfg.S, cfg.Sseg,
+            cfg.Pd, (int)N, qlen_d, ctx->flag_d, dc, de, trace ? ds : nullptr, fix_d, cfg.half);
         CK(cudaGetLastError());
         g_launches++;
         s = spec_fixup(ctx, xd, Z, N, rg.off, fix_d, dc, de, trace ? ds : nullptr, st);

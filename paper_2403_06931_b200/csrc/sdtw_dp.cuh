@@ -38,6 +38,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <type_traits>
 
 // Build-time knobs (A/B variants via -D; the defaults are the measured best)
@@ -1152,14 +1153,17 @@ static __global__ void finalize_kernel(const Partial* __restrict__ cand, int Z, 
 // candidate is ambiguous too: on strictly-won cells the winner's start is the true one,
 // on ties the priority rule of the merged DP decides.  A query with a
 // segment not overtaken (or such a tie) is marked for recomputation (fix[q] = 1).
-static __global__ void finalize_spec_kernel(const Partial* __restrict__ cand, const float* __restrict__ bnd_g, int Z,
+static __global__ void finalize_spec_kernel(const Partial* __restrict__ cand, const void* __restrict__ bnd_v, int Z,
                                             int S, int Sg, int PdMax, int N, const int* qlen, const int* err_flag,
-                                            float* out_cost, int64_t* out_end, int64_t* out_start, int* fix) {
+                                            float* out_cost, int64_t* out_end, int64_t* out_start, int* fix,
+                                            int half = 0) {
     const int q = blockIdx.x;
     if (q >= Z || *err_flag) return;
     if (qlen) N = qlen[q];                                 // ragged batch: this query's rows
     const bool trace = out_start != nullptr;
     const int es = trace ? 2 : 1;                          // floats per boundary entry
+    const float* bnd_g = static_cast<const float*>(bnd_v);
+    const __half* bnd_h = static_cast<const __half*>(bnd_v);   // packed-half kernel: binary16 entries
     const Partial* cq = cand + (long)q * S;
     Partial b = cq[0];
     for (int k = 1; k < 2 * Sg; ++k) {
@@ -1169,11 +1173,11 @@ static __global__ void finalize_spec_kernel(const Partial* __restrict__ cand, co
     Partial bc{INFINITY, 0x7fffffff, 0, 0};                // best correction candidate
     int undominated = 0;
     for (int s = 1; s < Sg; ++s) {
-        const float* a = bnd_g + ((long)q * S + s) * PdMax * es;
-        const float* c = bnd_g + ((long)q * S + 2 * Sg + s - 1) * PdMax * es;
+        const long ao = ((long)q * S + s) * PdMax, co = ((long)q * S + 2 * Sg + s - 1) * PdMax;
         int lt = 0;
         for (int r = threadIdx.x; r < N; r += blockDim.x) {
-            const float av = a[(long)r * es], cv = c[(long)r * es];
+            const float av = half ? __half2float(bnd_h[ao + r]) : bnd_g[(ao + r) * es];
+            const float cv = half ? __half2float(bnd_h[co + r]) : bnd_g[(co + r) * es];
             lt |= trace ? !(cv > av || (cv == INFINITY && av == INFINITY)) : cv < av;
         }
         lt = __syncthreads_or(lt);

@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(256, 2) sdtw_dp16_kernel(const DpParams P) {
     int* unit_sh = pp + 64;
     for (int unit_iter = 0;; ++unit_iter) {
     int q, seg = 0, pa = 0, pb = P.Pr;
+    int in_k = -1;                                  // speculative segments (sdtw_dp.cuh, DpParams::utab)
+    __half zrow = HZERO;                            // virtual row -1 (+inf: no free start)
     if (P.persistent) {
         if (threadIdx.x == 0) {
             const int raw = atomicAdd(P.counter, 1);
@@ -134,11 +136,19 @@ __global__ void __launch_bounds__(256, 2) sdtw_dp16_kernel(const DpParams P) {
         if (u >= P.Z * P.S) break;
         q = u % P.Z;
         seg = u / P.Z;
-        pa = (int)((long)seg * P.Pr / P.S);
-        pb = (int)((long)(seg + 1) * P.Pr / P.S);
-        if (seg > 0) {
+        int wait_slot = -1, wait_val = 0;
+        if (P.utab) {
+            const int4 d = P.utab[seg];
+            pa = d.x; pb = d.y; in_k = d.z; zrow = d.w ? HINF : HZERO;
+            if (in_k >= 0) { wait_slot = q * P.S + in_k; wait_val = 1; }
+        } else {
+            pa = (int)((long)seg * P.Pr / P.S);
+            pb = (int)((long)(seg + 1) * P.Pr / P.S);
+            if (seg > 0) { wait_slot = q; wait_val = seg; }
+        }
+        if (wait_slot >= 0) {
             long n = 0;
-            while (ld_acquire_gpu(P.seg_done + q) < seg) {
+            while (ld_acquire_gpu(P.seg_done + wait_slot) < wait_val) {
                 __nanosleep(256);
                 if (++n == (1LL << 26)) { printf("sdtw16 watchdog: unit %d waits segment\n", u); __trap(); }
             }
@@ -159,13 +169,15 @@ __global__ void __launch_bounds__(256, 2) sdtw_dp16_kernel(const DpParams P) {
     const int Mtot_bands = Pl * Pd;
 
     // prologue: query rows -> half2 (x_r, x_{r-1}) words, boundary ring, counters
-    const __half* bg = reinterpret_cast<const __half*>(P.bnd_g) + (long)q * PdMax;
+    const bool spec = P.utab != nullptr;
+    const __half* bg = reinterpret_cast<const __half*>(P.bnd_g) + (spec ? (long)q * P.S + max(in_k, 0) : (long)q) * PdMax;
+    const bool bnd_in = spec ? in_k >= 0 : pa > 0;
     for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
         const int rp = (r >= 1) ? r - 1 : r - 1 + Pd;
         const __half a = __float2half_rn((r < N) ? xq[r] : 0.0f);
         const __half b = __float2half_rn((rp < N) ? xq[rp] : 0.0f);
         xs[xrow_index(r, Pd, 2)] = h2_bits(__halves2half2(a, b));
-        bnd[r] = (pa > 0) ? bg[r] : HINF;
+        bnd[r] = bnd_in ? bg[r] : HINF;
     }
     if (threadIdx.x < 64) infs[threadIdx.x] = HINF;
     if (threadIdx.x < 32) {
@@ -225,8 +237,8 @@ __global__ void __launch_bounds__(256, 2) sdtw_dp16_kernel(const DpParams P) {
 #pragma unroll
                 for (int w = 0; w < WC; ++w) Yh[w] = h2_with(Yh[w], c, __float2half_rn(ys[w]));
 #pragma unroll
-                for (int k = 0; k < U; ++k) R.D[k] = h2_with(R.D[k], c, HZERO);
-                pdv = h2_with(pdv, c, HZERO);
+                for (int k = 0; k < U; ++k) R.D[k] = h2_with(R.D[k], c, zrow);
+                pdv = h2_with(pdv, c, zrow);
             }
         }
         pd = pdv;
@@ -374,14 +386,15 @@ __global__ void __launch_bounds__(256, 2) sdtw_dp16_kernel(const DpParams P) {
         }
     }
     if (P.persistent) {
-        if (seg + 1 < P.S) {
-            __half* bo = reinterpret_cast<__half*>(P.bnd_g) + (long)q * PdMax;
+        if (spec || seg + 1 < P.S) {
+            __half* bo = reinterpret_cast<__half*>(P.bnd_g) + (spec ? (long)q * P.S + seg : (long)q) * PdMax;
             for (int r = threadIdx.x; r < Pd; r += blockDim.x) bo[r] = bnd[r];
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
-            st_release_gpu(P.seg_done + q, seg + 1);
+            if (spec) st_release_gpu(P.seg_done + q * P.S + seg, 1);
+            else st_release_gpu(P.seg_done + q, seg + 1);
         }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");

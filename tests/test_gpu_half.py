@@ -102,3 +102,22 @@ def test_half_rejects_traceback_and_clusters():
         with sd.options(OPT_CLUSTER=2):
             with pytest.raises(sd.SdtwError):
                 sd.batch(np.ones((2, 10), np.float32))
+
+
+def test_half_speculative_small_batch_and_recompute():
+    """Speculative segments in packed half: a small batch bit-exact against
+    the half oracle and identical to sequential segments; queries copying the reference
+    across segment boundaries force failed corrections and recomputation, still exact."""
+    Q, Y = _inputs(6, 300, 200_000, 45)
+    c, e = _gpu16(Q, Y, OPT_SCHED=3)
+    _check(Q, Y, c, e)
+    c2, e2 = _gpu16(Q, Y, OPT_SCHED=2, OPT_SEGMENTS=3)
+    assert np.array_equal(c.view(np.uint32), c2.view(np.uint32)) and np.array_equal(e, e2)
+    M, N, Sg = 100_000, 1500, 8
+    Y = oracle.znorm(nanopore_reference(M, 46)[None])[0]
+    Pr = -(-M // 960)
+    bounds = [(s * Pr // Sg) * 960 for s in range(1, 4)]
+    Q = np.stack([Y[b - 200:b + N - 200] for b in bounds]).astype(np.float32)
+    c, e = _gpu16(Q, Y, OPT_SCHED=3, OPT_LANES=1, OPT_SPEC_ROUNDS=1, OPT_SEGMENTS=Sg)
+    assert sd.spec_recomputed() == len(bounds)
+    _check(Q, Y, c, e)
