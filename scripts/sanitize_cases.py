@@ -12,7 +12,8 @@ Q = nanopore_queries(8, 300, 20_000, 1)
 sd.set_reference(torch.as_tensor(Y, device=dev))
 Qt = torch.as_tensor(Q, device=dev)
 runs = [dict(), dict(OPT_PACKED=0, OPT_SEGMENT_W=15, OPT_LANES=2), dict(OPT_PACKED=2, OPT_SEGMENT_W=28),
-        dict(OPT_CLUSTER=2, OPT_LANES=2), dict(OPT_SCHED=2, OPT_SEGMENTS=3), dict(OPT_PACKED=3)]
+        dict(OPT_CLUSTER=2, OPT_LANES=2), dict(OPT_SCHED=2, OPT_SEGMENTS=3), dict(OPT_PACKED=3),
+        dict(OPT_SCHED=3, OPT_LANES=1), dict(OPT_SCHED=3, OPT_LANES=1, OPT_SPEC_ROUNDS=1, OPT_SEGMENTS=8)]
 for cfg in runs:
     with sd.options(**cfg):
         sd.batch(Qt)
@@ -20,5 +21,9 @@ for cfg in runs:
 sd.path(Qt[:4])
 off = np.array([0, 100, 350, 360, 900], np.int64)
 sd.batch_ragged(Qt.reshape(-1)[:900], off, start=True)
+with sd.options(OPT_SCHED=3, OPT_LANES=1):
+    sd.batch_ragged(Qt.reshape(-1)[:900], off, start=True)
+with sd.options(OPT_PRECISION=16, OPT_SCHED=3, OPT_LANES=1):
+    sd.batch(Qt)
 torch.cuda.synchronize()
 print("sanitize cases done")
