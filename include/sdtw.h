@@ -131,6 +131,35 @@ sdtw_status sdtw_path(const float* Q, int64_t n_queries, int64_t N,
                       float* out_cost, int64_t* out_end, int64_t* out_start,
                       int32_t* path_lo, int32_t* path_hi);
 
+/* Reference split across GPUs ("an exact reference split ...
+ * boundary columns passed between GPUs").  Building blocks for
+ * paper_2403_06931_b200.distributed.reference_split_batch: each rank holds one slice of
+ * the (globally normalised) reference and these two calls; the Python layer exchanges the
+ * columns with one all-gather.  fp32 cost/end only, fixed-length queries, no clusters.
+ *
+ * sdtw_round_columns: *cols = reference columns per DP round for queries of length N
+ * under the current options (slice lengths and n_cols below are multiples of it).
+ *
+ * sdtw_batch_columns: sdtw_batch over the current reference (speculative schedule) that
+ * also returns, for every query, the DP column at reference column *check_cols - 1
+ * (col_check, the free DP: start anywhere in this reference, +inf left of it) and at the
+ * last column M-1 (col_last; M must be a multiple of sdtw_round_columns).  Columns are
+ * n_queries x N fp32 row-major DEVICE buffers (either may be NULL).
+ *
+ * sdtw_boundary_dp: the DP over reference columns [0, n_cols) (0 = all; else a multiple of
+ * sdtw_round_columns) with left boundary column `boundary` (n_queries x N fp32, device;
+ * NULL = +inf) and the free start in row 0 when free_start != 0 (else no path may start
+ * here: virtual row -1 = +inf).  Returns the last-row minimum over those columns
+ * (out_cost, out_end: smallest argmin; +inf / 0 when no path reaches it) and, if col_out
+ * != NULL, the column n_cols - 1 (device, n_queries x N).  One DP unit per query.
+ * Errors: SDTW_E_ARG (start index, ragged, half, clusters, dual-query, too few rounds for
+ * the speculative schedule, bad n_cols, host column pointers), plus those of sdtw_batch. */
+sdtw_status sdtw_round_columns(int64_t N, int64_t* cols);
+sdtw_status sdtw_batch_columns(const float* Q, int64_t n_queries, int64_t N, float* out_cost, int64_t* out_end,
+                               float* col_check, float* col_last, int64_t* check_cols);
+sdtw_status sdtw_boundary_dp(const float* Q, int64_t n_queries, int64_t N, const float* boundary, int free_start,
+                             int64_t n_cols, float* out_cost, int64_t* out_end, float* col_out);
+
 /* z-normalisation of n_series contiguous series of length len (the paper's
  * runNormalizer; Eq. 2 P:L73 with the population variance of P:L85-L86):
  * fp64 accumulation, z = fl32((x - mean)/sd); degenerate series (var <= 1e-12 *

@@ -43,11 +43,17 @@ _lib.sdtw_set_option.argtypes = [ctypes.c_int, _i64]
 _lib.sdtw_get_option.argtypes = [ctypes.c_int, ctypes.POINTER(_i64)]
 _lib.sdtw_profile.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]
 _lib.sdtw_spec_recomputed.argtypes = [ctypes.POINTER(_i64)]
+_lib.sdtw_round_columns.argtypes = [_i64, ctypes.POINTER(_i64)]
+_lib.sdtw_batch_columns.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.POINTER(_i64)]
+_lib.sdtw_boundary_dp.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_int, _i64, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_void_p]
 _lib.sdtw_launch_count.restype = _i64
 _lib.sdtw_last_error.restype = ctypes.c_char_p
 _lib.sdtw_version.restype = ctypes.c_int
 for _n in ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
-           "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_spec_recomputed"):
+           "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_spec_recomputed", "sdtw_round_columns",
+           "sdtw_batch_columns", "sdtw_boundary_dp"):
     getattr(_lib, _n).restype = ctypes.c_int
 
 # ABI constants (include/sdtw.h)
@@ -60,6 +66,7 @@ _STATUS = {0: "SDTW_OK", 1: "SDTW_E_ARG", 2: "SDTW_E_NOREF", 3: "SDTW_E_CUDA", 4
 
 EXPORTED_SYMBOLS = ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
                     "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_spec_recomputed", "sdtw_launch_count",
+                    "sdtw_round_columns", "sdtw_batch_columns", "sdtw_boundary_dp",
                     "sdtw_last_error", "sdtw_release", "sdtw_version")
 
 
@@ -153,6 +160,50 @@ def batch(Q):
     _bind_stream(keep)
     _check(_lib.sdtw_batch(ctypes.c_void_p(ptr), Z, N, ctypes.c_void_p(pc), ctypes.c_void_p(pe)))
     return cost, end
+
+
+def round_columns(N: int) -> int:
+    """sdtw_round_columns: reference columns per DP round for queries of length N."""
+    n = _i64()
+    _check(_lib.sdtw_round_columns(int(N), ctypes.byref(n)))
+    return int(n.value)
+
+
+def batch_columns(Q, last: bool = True):
+    """sdtw_batch_columns (device tensors only): Q [Z, N] -> (cost, end, col_check [Z, N],
+    col_last [Z, N], check_cols): the free DP's column at reference column check_cols - 1
+    and at the last column."""
+    torch = _torch()
+    Z, N = Q.shape
+    col_check = torch.empty((Z, N), dtype=torch.float32, device=Q.device)
+    col_last = torch.empty((Z, N), dtype=torch.float32, device=Q.device) if last else None
+    keep, ptr, _ = _as_f32(Q)
+    cost, end, _, (pc, pe, _) = _outputs(keep, Z, False)
+    n = _i64()
+    _bind_stream(keep)
+    _check(_lib.sdtw_batch_columns(ctypes.c_void_p(ptr), Z, N, ctypes.c_void_p(pc), ctypes.c_void_p(pe),
+                                   ctypes.c_void_p(col_check.data_ptr()),
+                                   ctypes.c_void_p(None if col_last is None else col_last.data_ptr()),
+                                   ctypes.byref(n)))
+    return cost, end, col_check, col_last, int(n.value)
+
+
+def boundary_dp(Q, boundary=None, free_start: bool = True, n_cols: int = 0, column: bool = True):
+    """sdtw_boundary_dp (device tensors only): the DP over reference columns [0, n_cols)
+    from the left boundary column `boundary` [Z, N] (None = +inf), with or without the free
+    start -> (cost, end, column n_cols-1 [Z, N] or None)."""
+    torch = _torch()
+    Z, N = Q.shape
+    keep, ptr, _ = _as_f32(Q)
+    bkeep = None if boundary is None else boundary.to(torch.float32).contiguous()
+    col = torch.empty((Z, N), dtype=torch.float32, device=Q.device) if column else None
+    cost, end, _, (pc, pe, _) = _outputs(keep, Z, False)
+    _bind_stream(keep)
+    _check(_lib.sdtw_boundary_dp(ctypes.c_void_p(ptr), Z, N,
+                                 ctypes.c_void_p(None if bkeep is None else bkeep.data_ptr()),
+                                 1 if free_start else 0, int(n_cols), ctypes.c_void_p(pc), ctypes.c_void_p(pe),
+                                 ctypes.c_void_p(None if col is None else col.data_ptr())))
+    return cost, end, col
 
 
 def traceback(Q):

@@ -439,14 +439,28 @@ std::vector<int> unit_order_weighted(int64_t R, int S, int64_t W, const std::vec
     return order;
 }
 
+// Reference-split requests (sdtw_batch_columns / sdtw_boundary_dp).
+struct SegReq {
+    int mode = 0;                  // 1: speculative batch + column copies; 2: one-unit boundary DP
+    float* col_check = nullptr;    // mode 1: free-DP column at the end of the first Rc rounds [Z][N]
+    float* col_last = nullptr;     // mode 1: last column of the reference [Z][N]
+    int64_t* check_cols = nullptr; // mode 1: Rc * columns per round
+    const float* bnd = nullptr;    // mode 2: left boundary column [Z][N] (device; nullptr = +inf)
+    int free_start = 1;            // mode 2: 0 = virtual row -1 is +inf
+    int64_t cols = 0;              // mode 2: reference columns to run (multiple of the round width; 0 = all)
+    float* col_out = nullptr;      // mode 2: end column [Z][N] (device) or nullptr
+};
+
 sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
-                      int64_t* out_start, bool trace, BatchDev* dev_out, Ragged rg);
+                      int64_t* out_start, bool trace, BatchDev* dev_out = nullptr, Ragged rg = Ragged(),
+                      const SegReq* sr = nullptr);
 
 // Speculative segments: queries whose correction pass was not overtaken within Rc rounds
 // (fix[q] != 0) are recomputed with sequential segments from their normalised rows and
 // their results replace the speculative ones.
 sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const std::vector<int64_t>* off,
-                       const int* fix_d, float* dc, int64_t* de, int64_t* ds, cudaStream_t st) {
+                       const int* fix_d, float* dc, int64_t* de, int64_t* ds, cudaStream_t st,
+                       float* col_last = nullptr) {
     std::vector<int> fix((size_t)Z);
     CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(fix.data(), fix_d, (size_t)Z * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -466,7 +480,7 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
         nmin2 = std::min(nmin2, n);
         nmax2 = std::max(nmax2, n);
     }
-    const size_t need = 5 * (size_t)F + (size_t)off2[F];           // (end, start, cost) per query + rows
+    const size_t need = 5 * (size_t)F + (size_t)off2[F] * (col_last ? 2 : 1);   // (end, start, cost) + rows (+ columns)
     sdtw_status s = grow(&ctx->ws_fix, &ctx->ws_fix_n, need);
     if (s != SDTW_OK) return s;
     int64_t* fe = reinterpret_cast<int64_t*>(ctx->ws_fix);
@@ -489,9 +503,21 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
     g_opt.sched = 1;                                  // one CTA per ring: no speculation again
     g_opt.stream = st;
     const int64_t fixed_before = F;
-    s = run_batch(rows, F, off ? nmax2 : N, fc, fe, ds ? fs : nullptr, ds != nullptr, nullptr, rg2);
+    float* fcol = rows + off2[F];
+    if (col_last) {                                   // also the true last column: one-unit DP per query
+        g_opt.sched = 3;
+        SegReq r2;
+        r2.mode = 2;
+        r2.col_out = fcol;
+        s = run_batch(rows, F, N, fc, fe, nullptr, false, nullptr, Ragged(), &r2);
+    } else {
+        s = run_batch(rows, F, off ? nmax2 : N, fc, fe, ds ? fs : nullptr, ds != nullptr, nullptr, rg2);
+    }
     g_opt = saved;
     if (s != SDTW_OK) return s;
+    if (col_last)
+        for (int64_t k = 0; k < F; ++k)
+            CK(cudaMemcpyAsync(col_last + idx[k] * N, fcol + k * N, (size_t)N * 4, cudaMemcpyDeviceToDevice, st));
     for (int64_t k = 0; k < F; ++k) {
         CK(cudaMemcpyAsync(dc + idx[k], fc + k, sizeof(float), cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(de + idx[k], fe + k, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
@@ -570,7 +596,7 @@ std::vector<int> spec_order(int64_t R, const std::vector<int4>& t, int64_t W, co
 }
 
 sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
-                      int64_t* out_start, bool trace, BatchDev* dev_out = nullptr, Ragged rg = Ragged()) {
+                      int64_t* out_start, bool trace, BatchDev* dev_out, Ragged rg, const SegReq* sr) {
     if (N < 1 || Z < 0) return fail(SDTW_E_ARG, "N must be >= 1 and n_queries >= 0");
     if (Z > 0 && (!Q || !out_cost || !out_end || (trace && !out_start)))
         return fail(SDTW_E_ARG, "NULL pointer");
@@ -590,6 +616,24 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     s = plan(*ctx, Z, N, trace, &cfg, rg.off ? &rg : nullptr);
     if (s != SDTW_OK) return s;
     if (rg.off && cfg.dual) return fail(SDTW_E_ARG, "ragged batches need OPT_PACKED in {0, 1, 2}");
+    const int smode = sr ? sr->mode : 0;
+    if (smode) {
+        if (!cfg.spec || trace || rg.off || cfg.half)
+            return fail(SDTW_E_ARG, "reference-split calls need fp32 cost/end, fixed-length queries and the "
+                                    "speculative schedule (no clusters, OPT_SCHED 0 or 3, >= 4(Rc+1) rounds)");
+        const int64_t cpr = 32LL * cfg.C * cfg.GW * cfg.WC;
+        if (smode == 1 && sr->col_last && ctx->M % cpr != 0)
+            return fail(SDTW_E_ARG, "the last column needs a reference length that is a multiple of the round width");
+        if (smode == 2) {
+            const int64_t cols = sr->cols > 0 ? sr->cols : cfg.Pr * cpr;
+            if (cols % cpr != 0 || cols > cfg.Pr * cpr)
+                return fail(SDTW_E_ARG, "n_cols must be a multiple of the round width and <= the reference");
+            cfg.Sseg = 0;
+            cfg.Rc = (int)(cols / cpr);                     // rounds of the single unit
+            cfg.S = 1;
+            cfg.workers = (int)std::min<int64_t>(cfg.workers, cfg.units);
+        }
+    }
 
     const int kq = ptr_kind(Q), kc = ptr_kind(out_cost), ke = ptr_kind(out_end);
     const int ks = trace ? ptr_kind(out_start) : 1;
@@ -677,6 +721,8 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.bnd_g = nullptr;
     p.cand = nullptr;
     p.utab = nullptr;
+    p.bnd_user = nullptr;
+    p.col_out = nullptr;
     int* fix_d = nullptr;
     ctx->last_fixups = 0;
     if (cfg.persistent) {
@@ -697,7 +743,9 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         p.bnd_g = static_cast<unsigned char*>(p.cand) + 16 * (size_t)Z * cfg.S;
         CK(cudaMemsetAsync(b, 0, 256 + done_b, st));
         if (cfg.spec) {
-            const std::vector<int4> tab = spec_table(cfg.Pr, cfg.Sseg, cfg.Rc);
+            const std::vector<int4> tab = smode == 2
+                ? std::vector<int4>{make_int4(0, cfg.Rc, sr->bnd ? -2 : -1, sr->free_start ? 0 : 1)}
+                : spec_table(cfg.Pr, cfg.Sseg, cfg.Rc);
             if (tab.size() > ctx->utab_n) {
                 if (ctx->utab_d) cudaFree(ctx->utab_d);
                 ctx->utab_d = nullptr;
@@ -711,7 +759,10 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         if (cfg.spec || rg.off || ctx->order_key[0] != (int64_t)R || ctx->order_key[1] != cfg.S ||
             ctx->order_key[2] != cfg.workers) {
             std::vector<int> ord;
-            if (cfg.spec) {
+            if (smode == 2) {
+                ord.resize(R);
+                for (size_t k = 0; k < R; ++k) ord[k] = (int)k;
+            } else if (cfg.spec) {
                 std::vector<double> w;
                 if (rg.off) {
                     w.resize(R);
@@ -741,16 +792,35 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         }
         p.order = ctx->order_d;
     }
+    p.bnd_user = smode == 2 ? sr->bnd : nullptr;
+    p.col_out = smode == 2 ? sr->col_out : nullptr;
     if (o.profile) CK(cudaEventRecord(ctx->ev0, st));
     s = launch_dp(cfg, o.fma != 0, trace, p, st);
     if (s != SDTW_OK) return s;
-    if (cfg.spec) {
+    if (smode == 2) {
+        sdtw::finalize_kernel<<<(unsigned)((Z + 127) / 128), 128, 0, st>>>(
+            static_cast<const sdtw::Partial*>(p.cand), (int)Z, 1, ctx->flag_d, dc, de, nullptr);
+        CK(cudaGetLastError());
+        g_launches++;
+    } else if (cfg.spec) {
         sdtw::finalize_spec_kernel<<<(unsigned)Z, 128, 0, st>>>(
             static_cast<const sdtw::Partial*>(p.cand), p.bnd_g, (int)Z, cfg.S, cfg.Sseg,
             cfg.Pd, (int)N, qlen_d, ctx->flag_d, dc, de, trace ? ds : nullptr, fix_d, cfg.half);
         CK(cudaGetLastError());
         g_launches++;
-        s = spec_fixup(ctx, xd, Z, N, rg.off, fix_d, dc, de, trace ? ds : nullptr, st);
+        if (smode == 1) {                                   // free-DP columns of kinds A_0 and B_{Sg-1}
+            const size_t pitch = (size_t)cfg.S * cfg.Pd * sizeof(float);
+            const float* bg = static_cast<const float*>(p.bnd_g);
+            if (sr->col_check)
+                CK(cudaMemcpy2DAsync(sr->col_check, (size_t)N * 4, bg, pitch, (size_t)N * 4, (size_t)Z,
+                                     cudaMemcpyDeviceToDevice, st));
+            if (sr->col_last)
+                CK(cudaMemcpy2DAsync(sr->col_last, (size_t)N * 4, bg + (size_t)(2 * cfg.Sseg - 1) * cfg.Pd, pitch,
+                                     (size_t)N * 4, (size_t)Z, cudaMemcpyDeviceToDevice, st));
+            if (sr->check_cols) *sr->check_cols = (int64_t)cfg.Rc * 32LL * cfg.C * cfg.GW * cfg.WC;
+        }
+        s = spec_fixup(ctx, xd, Z, N, rg.off, fix_d, dc, de, trace ? ds : nullptr, st,
+                       smode == 1 ? sr->col_last : nullptr);
         if (s != SDTW_OK) return s;
     } else if (cfg.persistent) {
         sdtw::finalize_kernel<<<(unsigned)((Z + 127) / 128), 128, 0, st>>>(
@@ -912,6 +982,53 @@ sdtw_status sdtw_set_reference(const float* Y, int64_t M) {
 sdtw_status sdtw_batch(const float* Q, int64_t n_queries, int64_t N, float* out_cost, int64_t* out_end) {
     std::lock_guard<std::mutex> lk(g_mu);
     return run_batch(Q, n_queries, N, out_cost, out_end, nullptr, false);
+}
+
+sdtw_status sdtw_batch_columns(const float* Q, int64_t n_queries, int64_t N, float* out_cost, int64_t* out_end,
+                               float* col_check, float* col_last, int64_t* check_cols) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((col_check && ptr_kind(col_check) != 1) || (col_last && ptr_kind(col_last) != 1))
+        return fail(SDTW_E_ARG, "column outputs must be device pointers on the current device");
+    SegReq r;
+    r.mode = 1;
+    r.col_check = col_check;
+    r.col_last = col_last;
+    r.check_cols = check_cols;
+    return run_batch(Q, n_queries, N, out_cost, out_end, nullptr, false, nullptr, Ragged(), &r);
+}
+
+sdtw_status sdtw_boundary_dp(const float* Q, int64_t n_queries, int64_t N, const float* boundary, int free_start,
+                             int64_t n_cols, float* out_cost, int64_t* out_end, float* col_out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((boundary && ptr_kind(boundary) != 1) || (col_out && ptr_kind(col_out) != 1))
+        return fail(SDTW_E_ARG, "boundary / column must be device pointers on the current device");
+    if (n_cols < 0) return fail(SDTW_E_ARG, "n_cols must be >= 0");
+    const Options saved = g_opt;
+    if (g_opt.sched == 0) g_opt.sched = 3;               // one unit per query on the speculative path
+    SegReq r;
+    r.mode = 2;
+    r.bnd = boundary;
+    r.free_start = free_start ? 1 : 0;
+    r.cols = n_cols;
+    r.col_out = col_out;
+    const sdtw_status s = run_batch(Q, n_queries, N, out_cost, out_end, nullptr, false, nullptr, Ragged(), &r);
+    g_opt = saved;
+    return s;
+}
+
+sdtw_status sdtw_round_columns(int64_t N, int64_t* cols) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!cols || N < 1) return fail(SDTW_E_ARG, "NULL pointer or N < 1");
+    Ctx* ctx;
+    sdtw_status s = get_ctx(&ctx);
+    if (s != SDTW_OK) return s;
+    Ctx probe = *ctx;                                    // the width does not depend on the reference:
+    probe.M = 1LL << 24;                                 // plan against a stand-in length
+    LaunchCfg cfg;
+    s = plan(probe, 1, N, false, &cfg);
+    if (s != SDTW_OK) return s;
+    *cols = 32LL * cfg.C * cfg.GW * cfg.WC;
+    return SDTW_OK;
 }
 
 sdtw_status sdtw_traceback(const float* Q, int64_t n_queries, int64_t N, float* out_cost, int64_t* out_end,

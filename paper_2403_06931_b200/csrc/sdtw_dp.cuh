@@ -92,6 +92,11 @@ struct DpParams {
     // +inf).  Every unit stores its end column at bnd_g[(q*S + k)*PdMax] and raises
     // seg_done[q*S + k]; see spec_table() in sdtw_api.cu.
     const int4* utab;
+    // boundary DP (sdtw_boundary_dp, utab entry with in_k == -2): the unit's left boundary
+    // column is bnd_user[q*N + r] (rows >= N: +inf); col_out (if set) receives the unit's
+    // end column, rows [0, N), at col_out[q*N + r] (fp32 cost/end kernels only)
+    const float* bnd_user;
+    float* col_out;
 };
 
 template <bool TRACE> struct Entry { float d; };
@@ -717,6 +722,9 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     const bool spec = SPEC && P.utab;
     const E* bg = reinterpret_cast<const E*>(P.bnd_g) + (spec ? ((long)q * P.S + max(in_k, 0)) : (long)q) * PdMax;
     const bool bnd_in = spec ? in_k >= 0 : pa > 0;
+    // warp 0's first-round inbox is +inf only at the very start of the reference without a
+    // caller-supplied boundary column (sdtw_boundary_dp starts at round 0 from one)
+    const bool lead_inf = pa == 0 && !(SPEC && in_k == -2);
     for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
         float* dst = XS ? xs + r : xs + (long)xrow_index(r, Pd, NC) * XC;
 #pragma unroll
@@ -729,7 +737,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         if (bnd_in) {
             e = bg[r];
         } else {
-            e.d = INFINITY;
+            e.d = (SPEC && in_k == -2 && r < N) ? P.bnd_user[(long)q * N + r] : INFINITY;
             if constexpr (TRACE) e.s = 0;
         }
         bnd[r] = e;
@@ -805,7 +813,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         if constexpr (TRACE) lins = __shfl_up_sync(FULL, ls.right_s[C - 1], 1);
         {
             E e = (gw == 0) ? in_w0[r0] : my_in[(t - 1) & (RS - 1)];
-            const bool inf_in = gw == 0 && p0 < 1 && pa == 0;    // first round of the first segment
+            const bool inf_in = gw == 0 && p0 < 1 && lead_inf;   // first round of the first segment
             if (lane == 0) {
                 lin = inf_in ? INFINITY : e.d;
                 if constexpr (TRACE) lins = inf_in ? 0 : e.s;
@@ -887,7 +895,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                 nf = min((lim - rw) / PS, (K - s) / PS);
             }
             if (nf > 0) {
-                const bool inf_in = gw == 0 && pw == 0 && pa == 0;
+                const bool inf_in = gw == 0 && pw == 0 && lead_inf;
 #pragma unroll 1
                 for (int f = 0; f < nf; ++f) {
                     const int tp = tg + f * PS;
@@ -986,7 +994,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                 const E* ib0;
                 const E* ib1;
                 if (gw == 0) {
-                    ib0 = (pw == 0 && pa == 0) ? infs : bnd + rw;
+                    ib0 = (pw == 0 && lead_inf) ? infs : bnd + rw;
                     ib1 = ib0 + 1;
                 } else {
                     ib0 = my_in + ((tg - 1) & (RS - 1));
@@ -1111,6 +1119,8 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
             E* bo = reinterpret_cast<E*>(P.bnd_g) + (spec ? (long)q * P.S + seg : (long)q) * PdMax;
             for (int r = threadIdx.x; r < Pd; r += blockDim.x) bo[r] = bnd[r];
         }
+        if (spec && P.col_out)
+            for (int r = threadIdx.x; r < N; r += blockDim.x) P.col_out[(long)q * N + r] = bnd[r].d;
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
