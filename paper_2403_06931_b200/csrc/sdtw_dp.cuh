@@ -673,6 +673,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     int in_k = -1;                                          // speculative: source kind of the boundary
     float zrow = 0.0f;                                      // virtual row -1 (+inf: no free start)
     constexpr bool SPEC = !CLUSTER || SDTW_SPEC_CLUSTER;    // speculative units: one CTA per ring
+    constexpr bool BDP = SPEC && !TRACE;                     // caller boundary / column (sdtw_boundary_dp)
     if ((!CLUSTER || SDTW_SPEC_CLUSTER == 2) && P.persistent) {
         if (threadIdx.x == 0) {
             const int raw = atomicAdd(P.counter, 1);
@@ -724,7 +725,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     const bool bnd_in = spec ? in_k >= 0 : pa > 0;
     // warp 0's first-round inbox is +inf only at the very start of the reference without a
     // caller-supplied boundary column (sdtw_boundary_dp starts at round 0 from one)
-    const bool lead_inf = pa == 0 && !(SPEC && in_k == -2);
+    const bool lead_inf = pa == 0 && !(BDP && in_k == -2);
     for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
         float* dst = XS ? xs + r : xs + (long)xrow_index(r, Pd, NC) * XC;
 #pragma unroll
@@ -737,7 +738,8 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         if (bnd_in) {
             e = bg[r];
         } else {
-            e.d = (SPEC && in_k == -2 && r < N) ? P.bnd_user[(long)q * N + r] : INFINITY;
+            if constexpr (BDP) e.d = (in_k == -2 && r < N) ? P.bnd_user[(long)q * N + r] : INFINITY;
+            else e.d = INFINITY;
             if constexpr (TRACE) e.s = 0;
         }
         bnd[r] = e;
@@ -1119,8 +1121,10 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
             E* bo = reinterpret_cast<E*>(P.bnd_g) + (spec ? (long)q * P.S + seg : (long)q) * PdMax;
             for (int r = threadIdx.x; r < Pd; r += blockDim.x) bo[r] = bnd[r];
         }
-        if (spec && P.col_out)
-            for (int r = threadIdx.x; r < N; r += blockDim.x) P.col_out[(long)q * N + r] = bnd[r].d;
+        if constexpr (BDP) {
+            if (spec && P.col_out)
+                for (int r = threadIdx.x; r < N; r += blockDim.x) P.col_out[(long)q * N + r] = bnd[r].d;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
