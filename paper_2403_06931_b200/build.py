@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     if out is None and not defines and not force and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
-    objdir = os.path.join(HERE, "build" if out is None else "build_variant")
+    objdir = os.path.join(HERE, "build" if out is None else
+                          "build_variant_" + os.path.splitext(os.path.basename(out))[0])
     os.makedirs(objdir, exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + ["-D" + d for d in defines]
 

@@ -45,6 +45,12 @@
 #ifndef SDTW_C4_MINB
 #define SDTW_C4_MINB 3           // resident 4-warp CTAs per SM the 4-chain kernels are sized for
 #endif
+#ifndef SDTW_BDP_TRACE
+#define SDTW_BDP_TRACE 0      // debugging: 1 compiles the (dead) caller-boundary code into start-index kernels
+#endif
+#ifndef SDTW_ALWAYS_WAIT
+#define SDTW_ALWAYS_WAIT 0    // debugging: 1 waits for the staged strips before every slow period
+#endif
 #ifndef SDTW_SPEC_CLUSTER
 #define SDTW_SPEC_CLUSTER 0   // debugging: 1 compiles the (dead) speculative-unit decode into cluster
                               // kernels too, 2 also the (dead) persistent-unit code
@@ -673,7 +679,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     int in_k = -1;                                          // speculative: source kind of the boundary
     float zrow = 0.0f;                                      // virtual row -1 (+inf: no free start)
     constexpr bool SPEC = !CLUSTER || SDTW_SPEC_CLUSTER;    // speculative units: one CTA per ring
-    constexpr bool BDP = SPEC && !TRACE;                     // caller boundary / column (sdtw_boundary_dp)
+    constexpr bool BDP = SPEC && (!TRACE || SDTW_BDP_TRACE); // caller boundary / column (sdtw_boundary_dp)
     if ((!CLUSTER || SDTW_SPEC_CLUSTER == 2) && P.persistent) {
         if (threadIdx.x == 0) {
             const int raw = atomicAdd(P.counter, 1);
@@ -942,7 +948,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
             } else {
                 const int hi = rw + PS - 1;
                 const bool hit0 = lo <= 0 || hi >= Pd;
-                    if (hit0) {                                  // a transition reads the staged strips
+                    if (hit0 || SDTW_ALWAYS_WAIT) {              // a transition reads the staged strips
                         asm volatile("cp.async.wait_all;" ::: "memory");
                         __syncwarp();
                     }
