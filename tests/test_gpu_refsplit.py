@@ -105,3 +105,28 @@ def test_boundary_dp_pieces_match_oracle():
         c2, e2, col = sd.boundary_dp(Qt, None, True, 10 * cw)
     ref = oracle.sdtw(Q, Y[:10 * cw])
     assert np.array_equal(c2.cpu().numpy(), ref["cost"]) and np.array_equal(e2.cpu().numpy(), ref["end"])
+
+
+def test_reference_split_calls_reject_bad_arguments():
+    import oracle
+    import paper_2403_06931_b200 as sd
+    from datagen import nanopore_queries, nanopore_reference
+    M = 3840 * 20
+    Y = oracle.znorm(nanopore_reference(M, 74)[None])[0]
+    Q = torch.as_tensor(oracle.znorm(nanopore_queries(3, 200, M, 74)), device="cuda")
+    with sd.options(OPT_NORMALIZE=0):
+        sd.set_reference(torch.as_tensor(Y, device="cuda"))
+        cw = sd.round_columns(200)
+        with pytest.raises(sd.SdtwError) as ei:
+            sd.boundary_dp(Q, None, True, cw + 1)                   # not a multiple of the round width
+        assert ei.value.status == sd.E_ARG
+        with pytest.raises(sd.SdtwError):
+            sd.boundary_dp(Q, None, True, M + cw)                   # past the reference
+        with sd.options(OPT_CLUSTER=2):
+            with pytest.raises(sd.SdtwError):
+                sd.batch_columns(Q)                                  # clusters keep sequential segments
+        sd.set_reference(torch.as_tensor(Y[:M - 5], device="cuda"))
+        with pytest.raises(sd.SdtwError):
+            sd.batch_columns(Q)                                      # last column needs whole rounds
+        c, e, ck, cl, n = sd.batch_columns(Q, last=False)
+        assert cl is None and torch.isfinite(ck).all()
