@@ -267,7 +267,7 @@ __device__ __forceinline__ int start_sel(float d, float u, float m, int sd, int 
         "setp.eq.f32 pd, %1, %3;\n\t"
         "selp.b32 %0, %5, %6, pu;\n\t"
         "selp.b32 %0, %4, %0, pd;\n\t}"
-        : "=r"(r)
+        : "=&r"(r)                 // early clobber: %0 is written before %4 is read
         : "f"(d), "f"(u), "f"(m), "r"(sd), "r"(su), "r"(sl));
     return r;
 }
