@@ -377,7 +377,10 @@ def main():
                 args.config, w["Z"], N, M, " (start index on)" if trace else ""),
                 "queries_per_gpu": w["Z_local"], "N": N, "M": M, "normalize": True, "fma": True,
                 "packed": packed, "l2": "flushed (256 MiB write) before every timed step",
-                "parallelism": "query-sharded x%d, reference replicated" % world},
+                "parallelism": "query-sharded x%d, reference replicated" % world,
+                "schedule": {0: "auto (speculative round-segments with exact correction, DESIGN.md §13)",
+                             1: "one CTA per ring", 2: "sequential round-segments",
+                             3: "speculative round-segments"}[sd.get_option(sd.OPT_SCHED)]},
             "gpu_launches": launches, "roofline": roof, "clocks": clocks,
             "gsps_eq3": gsps(float(w["Z"]) * N, tot_ms / args.steps),
             "e2e": e2e, "cpu_baseline": cpu,
