@@ -172,3 +172,20 @@ def test_spec_errors():
         with pytest.raises(sd.SdtwError) as ei:
             sd.batch(bad)
         assert ei.value.status == sd.E_NONFINITE
+
+
+@pytest.mark.parametrize("Z,N,M,start", [(1, 2000, 10_000_000, False), (1, 500, 2_000_000, True),
+                                         (2048, 300, 1_000_000, False), (3, 8000, 3_000_000, False),
+                                         (700, 64, 500_000, True)])
+def test_spec_edge_shapes_identical_to_sequential(Z, N, M, start):
+    """One query (hundreds of segments), thousands of queries (two segments), single-row
+    layout (N=8,000), short queries with start index: bit-identical to sequential segments."""
+    Y = torch.from_numpy(nanopore_reference(M, 5)).to(DEV)
+    Q = torch.from_numpy(nanopore_queries(Z, N, M, 5)).to(DEV)
+    sd.set_reference(Y)
+    run = sd.traceback if start else sd.batch
+    with sd.options(OPT_SCHED=3):
+        a = [t.cpu() for t in run(Q)]
+    with sd.options(OPT_SCHED=2):
+        b = [t.cpu() for t in run(Q)]
+    assert all(torch.equal(x, y) for x, y in zip(a, b))
