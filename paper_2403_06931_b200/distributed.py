@@ -142,6 +142,12 @@ class CudaSplitOps:
         with self.sd.options(OPT_NORMALIZE=0):
             return self.sd.boundary_dp(Q, boundary, free_start=free_start, n_cols=n_cols)
 
+    def normalize(self, Q, Y):
+        """Per-query and whole-reference z-normalisation on the GPU (sdtw_znormalize):
+        the slices must share the global statistics of the reference."""
+        Yd = torch.as_tensor(np.asarray(Y, np.float32), device=Q.device)
+        return self.sd.znormalize(Q), self.sd.znormalize(Yd).cpu().numpy()
+
 
 def split_bounds(M: int, world: int, cols: int):
     """Slice [lo, hi) of every rank: equal multiples of the round width, the last takes the rest."""
@@ -162,14 +168,17 @@ def _comm_device(group, dev):
     return dev
 
 
-def reference_split_batch(Q: torch.Tensor, Y, ops=None, group=None):
-    """Exact sDTW of all queries Q [Z, N] (already normalised) against the reference Y
-    (already normalised, length M), the reference split over the ranks of `group`.
+def reference_split_batch(Q: torch.Tensor, Y, ops=None, group=None, normalize: bool = False):
+    """Exact sDTW of all queries Q [Z, N] against the reference Y (length M), the reference
+    split over the ranks of `group`.  Inputs are taken as already z-normalised unless
+    `normalize` (then each query and the whole reference are normalised first, on the GPU).
     Returns (cost fp32 [Z], end int64 [Z]) as numpy on every rank, plus the number of
     queries that needed the exact fallback chain."""
     if ops is None:
         import paper_2403_06931_b200 as sd
         ops = CudaSplitOps(sd)
+    if normalize:
+        Q, Y = ops.normalize(Q, Y)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     Z, N = Q.shape

@@ -130,3 +130,18 @@ def test_reference_split_calls_reject_bad_arguments():
             sd.batch_columns(Q)                                      # last column needs whole rounds
         c, e, ck, cl, n = sd.batch_columns(Q, last=False)
         assert cl is None and torch.isfinite(ck).all()
+
+
+def test_reference_split_normalises_raw_inputs():
+    """normalize=True on raw inputs equals the whole-reference batch with OPT_NORMALIZE=1
+    (world size 1: one slice, no exchange)."""
+    import paper_2403_06931_b200 as sd
+    from datagen import nanopore_queries, nanopore_reference
+    from paper_2403_06931_b200.distributed import reference_split_batch
+    M = 3840 * 40
+    Y = nanopore_reference(M, 75)
+    Q = torch.as_tensor(nanopore_queries(6, 500, M, 75), device="cuda")
+    cost, end, fb = reference_split_batch(Q, Y, normalize=True)
+    sd.set_reference(torch.as_tensor(Y, device="cuda"))
+    c, e = sd.batch(Q)
+    assert np.array_equal(cost, c.cpu().numpy()) and np.array_equal(end, e.cpu().numpy()) and fb == 0
