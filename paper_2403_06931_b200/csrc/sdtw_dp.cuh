@@ -51,6 +51,15 @@
 #ifndef SDTW_ALWAYS_WAIT
 #define SDTW_ALWAYS_WAIT 0    // debugging: 1 waits for the staged strips before every slow period
 #endif
+#ifndef SDTW_MOV_ASM
+// float-pair helpers: 3 (default) inline-PTX unpack + C++ pack; 0 all C++ (+4 registers,
+// -3.7 %); 1 the old inline-PTX pack `mov.b64 %0, {%1, %2}` (wrong cells in some layouts
+// and at ptxas -O1); 2 / 4 further debugging variants
+#define SDTW_MOV_ASM 3
+#endif
+#ifndef SDTW_SCALAR_CELL2
+#define SDTW_SCALAR_CELL2 0   // debugging: 1 computes the packed cells with scalar FADD / FFMA
+#endif
 #ifndef SDTW_SPEC_CLUSTER
 #define SDTW_SPEC_CLUSTER 0   // debugging: 1 compiles the (dead) speculative-unit decode into cluster
                               // kernels too, 2 also the (dead) persistent-unit code
@@ -217,6 +226,62 @@ __device__ __forceinline__ void wait_uniform(const int* pa, int na, bool ra, con
 }
 
 // ------------------------------------------------------------ arithmetic
+#if SDTW_MOV_ASM == 3 || SDTW_MOV_ASM == 4
+// 3 (default): inline-PTX unpack (register-pair halves, no instructions) + C++ pack (bit
+// casts and shift/or, which ptxas turns into the same pair move).  The inline-PTX PACK
+// `mov.b64 %0, {%1, %2}` gave wrong packed cells at ptxas -O1 (22 parity failures) and in
+// some -O3 code layouts (two-chain cluster and four-chain start-index kernels); with the
+// C++ pack every layout tried is exact, at 0.7 % of config-3 throughput.
+// 4 (debugging): C++ unpack + inline-PTX pack -- fails like 1.
+#if SDTW_MOV_ASM == 3
+__device__ __forceinline__ float lo32(unsigned long long r) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float hi32(unsigned long long r) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    return b;
+}
+__device__ __forceinline__ unsigned long long pk(float a, float b) {
+    return ((unsigned long long)__float_as_uint(b) << 32) | __float_as_uint(a);
+}
+#else
+__device__ __forceinline__ float lo32(unsigned long long r) { return __uint_as_float((unsigned)(r & 0xffffffffu)); }
+__device__ __forceinline__ float hi32(unsigned long long r) { return __uint_as_float((unsigned)(r >> 32)); }
+__device__ __forceinline__ unsigned long long pk(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+#endif
+#elif SDTW_MOV_ASM == 2
+// typed register-pair moves: mov.b64 between one .b64 and two .b32 registers (bit casts
+// on the C++ side), so ptxas sees plain 32-bit halves of a 64-bit register pair
+__device__ __forceinline__ float lo32(unsigned long long r) {
+    unsigned a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(r));
+    return __uint_as_float(a);
+}
+__device__ __forceinline__ float hi32(unsigned long long r) {
+    unsigned a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(r));
+    return __uint_as_float(b);
+}
+__device__ __forceinline__ unsigned long long pk(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(__float_as_uint(a)), "r"(__float_as_uint(b)));
+    return r;
+}
+#elif !SDTW_MOV_ASM
+// all C++ (bit casts + shifts): exact in every layout tried, 4 more registers
+__device__ __forceinline__ float lo32(unsigned long long r) { return __uint_as_float((unsigned)(r & 0xffffffffu)); }
+__device__ __forceinline__ float hi32(unsigned long long r) { return __uint_as_float((unsigned)(r >> 32)); }
+__device__ __forceinline__ unsigned long long pk(float a, float b) {
+    return ((unsigned long long)__float_as_uint(b) << 32) | __float_as_uint(a);
+}
+#else
 __device__ __forceinline__ float lo32(unsigned long long r) {
     float a, b;
     asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
@@ -232,6 +297,7 @@ __device__ __forceinline__ unsigned long long pk(float a, float b) {
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
     return r;
 }
+#endif
 __device__ __forceinline__ float min3f(float a, float b, float c) { return fminf(fminf(a, b), c); }
 
 // fp32 cell value d(x,y) + m (the oracle's `cell`), scalar
@@ -246,6 +312,14 @@ template <bool FMA>
 __device__ __forceinline__ unsigned long long cell2(unsigned long long xx, unsigned long long yy, float m0,
                                                     float m1) {
     unsigned long long tt, vv;
+#if SDTW_SCALAR_CELL2
+    // debugging: the same arithmetic with scalar FADD / FFMA (no f32x2 instructions)
+    {
+        const float t0 = __fsub_rn(lo32(xx), lo32(yy)), t1 = __fsub_rn(hi32(xx), hi32(yy));
+        if (FMA) return pk(__fmaf_rn(t0, t0, m0), __fmaf_rn(t1, t1, m1));
+        return pk(__fadd_rn(__fmul_rn(t0, t0), m0), __fadd_rn(__fmul_rn(t1, t1), m1));
+    }
+#endif
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(xx), "l"(yy));
     if (FMA) {
         asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(vv) : "l"(tt), "l"(pk(m0, m1)));

@@ -1,0 +1,9 @@
+#!/bin/bash
+cp paper_2403_06931_b200/libsdtw.so /tmp/cur.so
+for v in h3 h4; do
+  cp variants/$v.so paper_2403_06931_b200/libsdtw.so
+  timeout 600 python bench.py --steps 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('BENCH $v', d['value'])"
+  cp variants/${v}_o1.so paper_2403_06931_b200/libsdtw.so
+  echo "== ${v}_o1"; timeout 600 python -m pytest tests/test_gpu_parity.py -q --tb=no 2>&1 | tail -1
+done
+cp /tmp/cur.so paper_2403_06931_b200/libsdtw.so

@@ -1,0 +1,7 @@
+#!/bin/bash
+cp paper_2403_06931_b200/libsdtw.so /tmp/cur.so
+for v in o1_orient1 o1_orient0 o1_slow; do
+  cp variants/$v.so paper_2403_06931_b200/libsdtw.so
+  echo "== $v"; timeout 600 python scripts/o1_probe.py 2>&1 | head -3
+done
+cp /tmp/cur.so paper_2403_06931_b200/libsdtw.so
