@@ -35,16 +35,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=(), extra=()) -> str:
     """Compile each translation unit to an object in parallel, then link libsdtw.so.
     ``out``/``defines`` build an experimental variant elsewhere (A/B runs only)."""
-    if out is None and not defines and not force and not _stale():
+    if out is None and not defines and not extra and not force and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
     objdir = os.path.join(HERE, "build" if out is None else
                           "build_variant_" + os.path.splitext(os.path.basename(out))[0])
     os.makedirs(objdir, exist_ok=True)
-    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + ["-D" + d for d in defines]
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + ["-D" + d for d in defines] + list(extra)
 
     def one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
@@ -64,8 +64,9 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
 
 
 if __name__ == "__main__":
-    # python build.py [--force] [--out PATH -DNAME=V ...]
+    # python build.py [--force] [--out PATH -DNAME=V ... --xflag=FLAG ...]
     args = sys.argv[1:]
     out = args[args.index("--out") + 1] if "--out" in args else None
     defs = [a[2:] for a in args if a.startswith("-D")]
-    print(build(force="--force" in args, verbose=True, out=out, defines=defs))
+    extra = [a[len("--xflag="):] for a in args if a.startswith("--xflag=")]
+    print(build(force="--force" in args, verbose=True, out=out, defines=defs, extra=extra))
