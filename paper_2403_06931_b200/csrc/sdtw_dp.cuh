@@ -226,7 +226,23 @@ __device__ __forceinline__ void wait_uniform(const int* pa, int na, bool ra, con
 }
 
 // ------------------------------------------------------------ arithmetic
-#if SDTW_MOV_ASM == 3 || SDTW_MOV_ASM == 4
+#if SDTW_MOV_ASM == 5
+// (experiment) PTX unpack + pack through a float2 / u64 reinterpretation
+__device__ __forceinline__ float lo32(unsigned long long r) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float hi32(unsigned long long r) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    return b;
+}
+__device__ __forceinline__ unsigned long long pk(float a, float b) {
+    const float2 f = make_float2(a, b);
+    return *reinterpret_cast<const unsigned long long*>(&f);
+}
+#elif SDTW_MOV_ASM == 3 || SDTW_MOV_ASM == 4
 // 3 (default): inline-PTX unpack (register-pair halves, no instructions) + C++ pack (bit
 // casts and shift/or, which ptxas turns into the same pair move).  The inline-PTX PACK
 // `mov.b64 %0, {%1, %2}` gave wrong packed cells at ptxas -O1 (22 parity failures) and in
