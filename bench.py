@@ -6,8 +6,10 @@ ranks.  One "step" = one pass of the whole hot path over one batch: query
 z-normalisation + wavefront DP + min/argmin epilogue (+ the one all-gather of
 per-query records when N>1), through the public API (sdtw_batch) on inputs
 already resident in HBM.  Default workload (`--config c3`): 512 x 2,000-sample
-queries per GPU against a 10M-sample synthetic nanopore-like reference
-(BASELINE configs 3 at 1 GPU; 4,096 queries at 8 GPUs = config 4), weak scaling.
+queries against a 10M-sample synthetic nanopore-like reference (BASELINE config 3),
+STRONG scaling: at N GPUs each rank takes 512/N queries (64 at N=8), the metric's
+"512x2000 queries, 1/2/4/8 B200".  `--scaling weak` keeps 512 queries per GPU
+(4,096 at 8 GPUs = config 4).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c4|c5_500|...]
                     [--impl ours|reference] [--scaling weak|strong]
@@ -58,6 +60,24 @@ def _traffic(config, w, precision=32):
         if (int(t["Z"]) == int(w["Z_local"]) and int(t["N"]) == w["N"] and int(t["M"]) == w["M"]
                 and int(t.get("precision", 32)) == precision):
             return float(t["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+def _issue_counts(config, w, precision=32):
+    """Measured instruction counts per cell of the DP kernel from the committed ncu capture of
+    this workload (profiles/issue_<config>.json, written by scripts/ncu_issue.py from
+    `ncu --set full` of one DP launch): issue slots per cell = warp instructions x 32 / cells,
+    thread instructions per cell, issue-active fraction.  None when no capture matches."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue_%s.json" % config)) as f:
+            t = json.load(f)
+        if (int(t["Z"]) == int(w["Z_local"]) and int(t["N"]) == w["N"] and int(t["M"]) == w["M"]
+                and int(t.get("precision", 32)) == precision):
+            return {"issue_slots_per_cell_ncu": t["issue_slots_per_cell"],
+                    "thread_inst_per_cell_ncu": t["thread_inst_per_cell"],
+                    "issue_active_ncu": t["issue_active"], "ncu_capture": t["source"]}
     except Exception:
         pass
     return None
@@ -184,10 +204,32 @@ def run_reference(args):
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic nanopore-like (datagen), seeded",
         "config": {"workload": args.config, "sample": sample},
-        "cpu_baseline": {"value": val, "unit": "GCUPS", "cores": threads, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "GCUPS", "cores": threads, "kind": "oracle", "sample": sample,
+                         "host": host_cpu()},
         "e2e": {"value": val, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def host_cpu():
+    """lscpu model name, sockets, physical cores and hardware threads of this host."""
+    info = {"model": None, "sockets": None, "cores": None, "threads": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                k, v = line.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["model"] = kv.get("Model name")
+        soc = int(kv.get("Socket(s)", "0") or 0)
+        cps = int(kv.get("Core(s) per socket", "0") or 0)
+        info["sockets"] = soc or None
+        info["cores"] = soc * cps or None
+        info["threads"] = int(kv.get("CPU(s)", info["threads"]) or info["threads"])
+    except Exception:
+        pass
+    return info
 
 
 def cpu_baseline_leg(args, Q, Y, N):
@@ -206,7 +248,7 @@ def cpu_baseline_leg(args, Q, Y, N):
     cells = float(nq) * N * Ms
     return {"value": cells / dt / 1e9, "unit": "GCUPS", "cores": threads, "kind": "oracle",
             "sample": "%d queries x %d vs first %d reference samples of the same inputs, %d threads, %.1f s"
-                      % (nq, N, Ms, threads, dt)}
+                      % (nq, N, Ms, threads, dt), "host": host_cpu()}
 
 
 def main():
@@ -216,7 +258,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--half", action="store_true",
@@ -239,8 +281,14 @@ def main():
     import torch.distributed as dist
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(), "rank": rank,
+                "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version())}
+        print("[bench] communicator: %s world_size=%d rank=%d local_rank=%d device=%s nccl=%s"
+              % (comm["backend"], comm["world_size"], rank, local, dev, comm["nccl_version"]),
+              file=sys.stderr, flush=True)
 
     import paper_2403_06931_b200 as sd
     from paper_2403_06931_b200.distributed import distributed_batch
@@ -278,6 +326,7 @@ def main():
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     dp_ms = []
+    recomputed = 0
     launches0 = sd.launch_count()
     sampler = ClockSampler(local)
     with sd.options(OPT_PROFILE=1), sampler:
@@ -290,6 +339,7 @@ def main():
             step()
             ev[i][1].record(stream)
             dp_ms.append(sd.profile()[0])
+            recomputed += sd.spec_recomputed()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -323,6 +373,9 @@ def main():
             "dp_kernel_ms": dp_avg}
     if clocks.get("sm_mhz"):
         roof["frac_at_sampled_clock"] = achieved / (peak * clocks["sm_mhz"] / fmax)
+    meas = _issue_counts(args.config, w, 16 if args.half else 32)
+    if meas:
+        roof.update(meas)
     if trace:
         # the start-index cell needs 5 ALU-pipe ops (FMNMX3 + 2 FSETP + 2 SEL; the ALU pipe
         # issues 16 lanes/clk/SMSP): that pipe, not issue, binds it (ncu: alu 72 % busy)
@@ -347,8 +400,8 @@ def main():
             # H2D copy, the kernels and the D2H result copy on this stream
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            if world > 1:
-                distributed_batch(Qh.numpy(), traceback=trace, pre_sharded=True, device=dev, path=args.path)
+            if world > 1:   # the gathered records stay on the GPU: read the costs back to the host
+                distributed_batch(Qh.numpy(), traceback=trace, pre_sharded=True, device=dev, path=args.path)[0].cpu()
             else:
                 api(Qh.numpy())
             e1.record(stream)
@@ -377,11 +430,13 @@ def main():
                 args.config, w["Z"], N, M, " (start index on)" if trace else ""),
                 "queries_per_gpu": w["Z_local"], "N": N, "M": M, "normalize": True, "fma": True,
                 "packed": packed, "l2": "flushed (256 MiB write) before every timed step",
-                "parallelism": "query-sharded x%d, reference replicated" % world,
+                "parallelism": "query-sharded x%d (%s scaling), reference replicated, one all-gather of "
+                               "per-query records" % (world, args.scaling),
                 "schedule": {0: "auto (speculative round-segments with exact correction, DESIGN.md §13)",
                              1: "one CTA per ring", 2: "sequential round-segments",
                              3: "speculative round-segments"}[sd.get_option(sd.OPT_SCHED)]},
             "gpu_launches": launches, "roofline": roof, "clocks": clocks,
+            "spec_recomputed": recomputed, "build": sd.build_info(), "comm": comm,
             "gsps_eq3": gsps(float(w["Z"]) * N, tot_ms / args.steps),
             "e2e": e2e, "cpu_baseline": cpu,
         }

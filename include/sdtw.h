@@ -160,6 +160,27 @@ sdtw_status sdtw_batch_columns(const float* Q, int64_t n_queries, int64_t N, flo
 sdtw_status sdtw_boundary_dp(const float* Q, int64_t n_queries, int64_t N, const float* boundary, int free_start,
                              int64_t n_cols, float* out_cost, int64_t* out_end, float* col_out);
 
+/* The two decisions of the reference split, on the device, so that the
+ * Python layer only moves columns and records:
+ *
+ * sdtw_columns_dominate: the overtaking test of the correction (DESIGN.md §13 "Why it is
+ * exact": once the boundary DP is >= the free DP on a whole column it stays so on every
+ * later column).  out_flag[q] = 1 iff B[q][i] >= F[q][i] for every row i < N, else 0.
+ * B, F: n_queries x N fp32 row-major; out_flag: n_queries int32.  All DEVICE pointers on
+ * the current device; returns after the flags are written.
+ *
+ * sdtw_merge_candidates: per query q, the lexicographic minimum of (cost, end) (PAPER.md
+ * P:L35, the last-row minimum; reading G5: smallest end on equal cost) over the n_sets
+ * candidate sets k whose valid[k][q] != 0 (valid == NULL: all valid).  cost / end /
+ * valid: n_sets x n_queries, set-major; a query whose best cost is +inf gets end 0.
+ * out_invalid (optional): 1 iff some set of that query was invalid (a correction that was
+ * not overtaken: the query needs the exact fallback chain), else 0.  All DEVICE pointers
+ * on the current device.  Errors: SDTW_E_ARG (n_sets < 1, negative sizes, NULL or host
+ * pointers), SDTW_E_CUDA. */
+sdtw_status sdtw_columns_dominate(const float* B, const float* F, int64_t n_queries, int64_t N, int32_t* out_flag);
+sdtw_status sdtw_merge_candidates(const float* cost, const int64_t* end, const int32_t* valid, int64_t n_sets,
+                                  int64_t n_queries, float* out_cost, int64_t* out_end, int32_t* out_invalid);
+
 /* z-normalisation of n_series contiguous series of length len (the paper's
  * runNormalizer; Eq. 2 P:L73 with the population variance of P:L85-L86):
  * fp64 accumulation, z = fl32((x - mean)/sd); degenerate series (var <= 1e-12 *
@@ -188,7 +209,13 @@ const char* sdtw_last_error(void);
 /* Free the current device's context (reference, workspaces). */
 void sdtw_release(void);
 
+/* ABI version (2: exact-sum normaliser, sdtw_build_info, the reference-split merge calls). */
 int sdtw_version(void);
+
+/* Static text naming the nvcc/ptxas version the library was built with (and the float-pair
+ * pack mode of the packed kernels), for bench lines and bug reports.  Owned
+ * by the library; never NULL. */
+const char* sdtw_build_info(void);
 
 #ifdef __cplusplus
 }

@@ -7,6 +7,7 @@ package ``paper_2403_06931_b200``. It shares no code with the CUDA path.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 
@@ -46,8 +47,6 @@ def lib():
         L.oracle_walkback_path.restype = ctypes.c_int
         L.oracle_round_half.argtypes = [ctypes.c_double, ctypes.c_double]
         L.oracle_round_half.restype = ctypes.c_float
-        L.oracle_znorm.argtypes = [f32p, i64, i64, f32p]
-        L.oracle_znorm.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -138,17 +137,33 @@ def sdtw_path(x, Y, fma: bool = True):
 
 
 def znorm(X):
-    """Per-series z-normalisation (Eq. 2), fp64 accumulation, fp32 out."""
+    """Per-series z-normalisation, §5.1 Eq. 2 with the statistics of the
+    quoted code: mean = sum/n, var = sumSq/n - mean^2 (population, reading
+    G7), S = sqrt(var), z = (x - mean)/S rounded once to fp32.  Reading G8: sum and sumSq
+    are the EXACT sums of the fp32 samples, each rounded once to fp64 (math.fsum is the
+    library's exactly rounded sum; x*x is exact in fp64 for an fp32 x), so the result does
+    not depend on any summation order.  Reading G9: var <= 1e-12*E[x^2] or sumSq == 0 ->
+    all zeros.  Every fp64 operation below is one IEEE-rounded numpy/Python operation."""
     X = np.asarray(X, dtype=np.float32)
     shape = X.shape
     if X.ndim == 1:
         X = X[None, :]
-    Xc, xp = _f32(X)
-    out = np.empty_like(Xc)
-    rc = lib().oracle_znorm(xp, Xc.shape[0], Xc.shape[1],
-                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
-    if rc != 0:
-        raise ValueError("oracle_znorm: bad arguments")
+    n_series, n = X.shape
+    if n < 1:
+        raise ValueError("znorm: series length must be >= 1")
+    out = np.empty((n_series, n), np.float32)
+    for q in range(n_series):
+        x = X[q].astype(np.float64)
+        s = math.fsum(x)
+        sumsq = math.fsum(x * x)
+        mean = s / n
+        ex2 = sumsq / n
+        var = ex2 - mean * mean
+        if sumsq == 0.0 or var <= 1e-12 * ex2:
+            out[q] = 0.0
+            continue
+        sd = math.sqrt(var)
+        out[q] = ((x - mean) / sd).astype(np.float32)
     return out.reshape(shape)
 
 

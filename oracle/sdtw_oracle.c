@@ -31,11 +31,8 @@
  *  Packed half (fma_mode == 2): the same recurrence with every value
  *  rounded to binary16 after each operation (oracle_round_half / oracle_cell16 below).
  *
- *  Normaliser, §5.1 Eq. 2 and the quoted code:
- *      mean = sum/n; var = sumSq/n - mean*mean; S = sqrt(var); z = (x-mean)/S
- *  population variance (reading G7), fp64 accumulation, one rounding to fp32
- *  (reading G8), degenerate series (var <= 1e-12 * sumSq/n, or sumSq == 0)
- *  map to all zeros (reading G9).
+ *  The normaliser (§5.1 Eq. 2) lives in oracle/__init__.py (znorm): its
+ *  sums are exact (math.fsum), which plain C fp64 accumulation is not (reading G8).
  *
  * Pins (tests/test_oracle_pins.py): SPEC worked examples, brute-force path
  * enumeration (tests/pins/brute.c), closed forms for N=1 / M=1 / constant
@@ -269,30 +266,4 @@ int oracle_walkback_path(const float* D, int64_t N, int64_t M, int64_t end, int6
 }
 
 /* z-normalisation of n_series contiguous series of length len (Eq. 2). */
-int oracle_znorm(const float* in, int64_t n_series, int64_t len, float* out)
-{
-    if (n_series < 0 || len < 1) return 1;
-    for (int64_t q = 0; q < n_series; ++q) {
-        const float* x = in + q * len;
-        float* z = out + q * len;
-        double sum = 0.0, sumsq = 0.0;
-        for (int64_t k = 0; k < len; ++k) {
-            double v = (double)x[k];
-            sum += v;
-            sumsq += v * v;
-        }
-        double n = (double)len;
-        double mean = sum / n;
-        double ex2 = sumsq / n;
-        double var = ex2 - mean * mean;
-        if (sumsq == 0.0 || var <= 1e-12 * ex2) {
-            for (int64_t k = 0; k < len; ++k) z[k] = 0.0f;
-            continue;
-        }
-        double sd = sqrt(var);
-        for (int64_t k = 0; k < len; ++k) z[k] = (float)(((double)x[k] - mean) / sd);
-    }
-    return 0;
-}
-
 int oracle_abi_version(void) { return 1; }

@@ -20,7 +20,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsdtw.so")
+# SDTW_LIB: load an experimental build of the same library from its own path (A/B and
+# alternate-layout parity runs) instead of overwriting the in-tree libsdtw.so
+LIB_PATH = os.environ.get("SDTW_LIB") or os.path.join(_HERE, "libsdtw.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -48,12 +50,16 @@ _lib.sdtw_batch_columns.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p
                                     ctypes.c_void_p, ctypes.POINTER(_i64)]
 _lib.sdtw_boundary_dp.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_int, _i64, ctypes.c_void_p,
                                   ctypes.c_void_p, ctypes.c_void_p]
+_lib.sdtw_columns_dominate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _i64, _i64, ctypes.c_void_p]
+_lib.sdtw_merge_candidates.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, _i64, _i64, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p]
 _lib.sdtw_launch_count.restype = _i64
 _lib.sdtw_last_error.restype = ctypes.c_char_p
 _lib.sdtw_version.restype = ctypes.c_int
+_lib.sdtw_build_info.restype = ctypes.c_char_p
 for _n in ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
            "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_spec_recomputed", "sdtw_round_columns",
-           "sdtw_batch_columns", "sdtw_boundary_dp"):
+           "sdtw_batch_columns", "sdtw_boundary_dp", "sdtw_columns_dominate", "sdtw_merge_candidates"):
     getattr(_lib, _n).restype = ctypes.c_int
 
 # ABI constants (include/sdtw.h)
@@ -67,7 +73,8 @@ _STATUS = {0: "SDTW_OK", 1: "SDTW_E_ARG", 2: "SDTW_E_NOREF", 3: "SDTW_E_CUDA", 4
 EXPORTED_SYMBOLS = ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
                     "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_spec_recomputed", "sdtw_launch_count",
                     "sdtw_round_columns", "sdtw_batch_columns", "sdtw_boundary_dp",
-                    "sdtw_last_error", "sdtw_release", "sdtw_version")
+                    "sdtw_columns_dominate", "sdtw_merge_candidates",
+                    "sdtw_last_error", "sdtw_release", "sdtw_version", "sdtw_build_info")
 
 
 class SdtwError(RuntimeError):
@@ -113,6 +120,11 @@ def _as_f32(x):
 
 def version() -> int:
     return int(_lib.sdtw_version())
+
+
+def build_info() -> str:
+    """sdtw_build_info: the nvcc/ptxas version the library was compiled with, and its pack mode."""
+    return _lib.sdtw_build_info().decode()
 
 
 def set_option(key: int, value: int):
@@ -204,6 +216,38 @@ def boundary_dp(Q, boundary=None, free_start: bool = True, n_cols: int = 0, colu
                                  1 if free_start else 0, int(n_cols), ctypes.c_void_p(pc), ctypes.c_void_p(pe),
                                  ctypes.c_void_p(None if col is None else col.data_ptr())))
     return cost, end, col
+
+
+def columns_dominate(B, F):
+    """sdtw_columns_dominate (device tensors [Z, N]): int32 [Z], 1 iff B >= F on every row."""
+    torch = _torch()
+    Bk = B.to(torch.float32).contiguous()
+    Fk = F.to(torch.float32).contiguous()
+    Z, N = Bk.shape
+    out = torch.empty(Z, dtype=torch.int32, device=Bk.device)
+    _bind_stream(Bk)
+    _check(_lib.sdtw_columns_dominate(ctypes.c_void_p(Bk.data_ptr()), ctypes.c_void_p(Fk.data_ptr()), Z, N,
+                                      ctypes.c_void_p(out.data_ptr())))
+    return out
+
+
+def merge_candidates(cost, end, valid=None):
+    """sdtw_merge_candidates (device tensors [n_sets, Z]): per query the lexicographic
+    (cost, end) minimum over the valid sets -> (cost [Z], end [Z], invalid [Z] int32)."""
+    torch = _torch()
+    ck = cost.to(torch.float32).contiguous()
+    ek = end.to(torch.int64).contiguous()
+    vk = None if valid is None else valid.to(torch.int32).contiguous()
+    S, Z = ck.shape
+    oc = torch.empty(Z, dtype=torch.float32, device=ck.device)
+    oe = torch.empty(Z, dtype=torch.int64, device=ck.device)
+    oi = torch.empty(Z, dtype=torch.int32, device=ck.device)
+    _bind_stream(ck)
+    _check(_lib.sdtw_merge_candidates(ctypes.c_void_p(ck.data_ptr()), ctypes.c_void_p(ek.data_ptr()),
+                                      ctypes.c_void_p(None if vk is None else vk.data_ptr()), S, Z,
+                                      ctypes.c_void_p(oc.data_ptr()), ctypes.c_void_p(oe.data_ptr()),
+                                      ctypes.c_void_p(oi.data_ptr())))
+    return oc, oe, oi
 
 
 def traceback(Q):

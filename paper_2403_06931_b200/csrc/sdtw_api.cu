@@ -99,7 +99,7 @@ sdtw_status get_ctx(Ctx** out) {
         CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
         CK(cudaMalloc(&c.flag_d, 16));
         CK(cudaHostAlloc(&c.flag_h, 16, cudaHostAllocDefault));
-        CK(cudaMalloc(&c.ws_part, sizeof(double) * (2 * 4096 + 8)));
+        CK(cudaMalloc(&c.ws_part, sizeof(double) * (4 * 4096 + 8)));   // 4 doubles per partial
         CK(cudaEventCreate(&c.ev0));
         CK(cudaEventCreate(&c.ev1));
         c.init = true;
@@ -723,6 +723,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.utab = nullptr;
     p.bnd_user = nullptr;
     p.col_out = nullptr;
+    p.negzero = -0.0f;
     int* fix_d = nullptr;
     ctx->last_fixups = 0;
     if (cfg.persistent) {
@@ -939,6 +940,38 @@ sdtw_status run_path(const float* Q, int64_t Z, int64_t N, float* out_cost, int6
     return SDTW_OK;
 }
 
+// ------------------------------------------------------------------ reference split
+// Overtaking test of a correction (DESIGN.md §13/§14): flag[q] = all rows B >= F.
+__global__ void dominate_kernel(const float* __restrict__ B, const float* __restrict__ F, int64_t N,
+                                int32_t* flag) {
+    const int64_t q = blockIdx.x;
+    int lt = 0;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) lt |= !(B[q * N + i] >= F[q * N + i]);
+    lt = __syncthreads_or(lt);
+    if (threadIdx.x == 0) flag[q] = lt ? 0 : 1;
+}
+
+// Lexicographic (cost, end) minimum over the valid candidate sets of each query.
+__global__ void merge_kernel(const float* __restrict__ cost, const int64_t* __restrict__ end,
+                             const int32_t* __restrict__ valid, int64_t n_sets, int64_t Z, float* out_cost,
+                             int64_t* out_end, int32_t* out_invalid) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Z) return;
+    float bc = INFINITY;
+    int64_t be = INT64_MAX;
+    int inv = 0;
+    for (int64_t k = 0; k < n_sets; ++k) {
+        if (valid && !valid[k * Z + q]) { inv = 1; continue; }
+        const float c = cost[k * Z + q];
+        const int64_t e = end[k * Z + q];
+        if (c < bc || (c == bc && e < be)) { bc = c; be = e; }
+    }
+    if (!(bc < INFINITY)) be = 0;                      // no path reaches the last row (or overflow)
+    out_cost[q] = bc;
+    out_end[q] = be;
+    if (out_invalid) out_invalid[q] = inv;
+}
+
 }  // namespace
 
 extern "C" {
@@ -960,11 +993,12 @@ sdtw_status sdtw_set_reference(const float* Y, int64_t M) {
                                     kind ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) { cudaFree(buf); return cuda_fail(e, "cudaMemcpyAsync(reference)"); }
     const int nparts = 1184;
-    cudaMemsetAsync(ctx->flag_d, 0, sizeof(int), st);
+    e = cudaMemsetAsync(ctx->flag_d, 0, sizeof(int), st);
+    if (e != cudaSuccess) { cudaFree(buf); return cuda_fail(e, "cudaMemsetAsync(flag)"); }
     sdtw::ref_partials_kernel<<<nparts, 256, 0, st>>>(buf, M, ctx->ws_part, ctx->flag_d);
-    sdtw::ref_stats_kernel<<<1, 256, 0, st>>>(ctx->ws_part, nparts, M, ctx->ws_part + 2 * 4096);
+    sdtw::ref_stats_kernel<<<1, 256, 0, st>>>(ctx->ws_part, nparts, M, ctx->ws_part + 4 * 4096);
     const int norm = g_opt.normalize;
-    sdtw::ref_apply_kernel<<<1184, 256, 0, st>>>(buf, M, Malloc, ctx->ws_part + 2 * 4096, norm, buf);
+    sdtw::ref_apply_kernel<<<1184, 256, 0, st>>>(buf, M, Malloc, ctx->ws_part + 4 * 4096, norm);   // in place
     g_launches += 3;
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -1216,6 +1250,45 @@ void sdtw_release(void) {
     c = Ctx();
 }
 
-int sdtw_version(void) { return 1; }
+sdtw_status sdtw_columns_dominate(const float* B, const float* F, int64_t n_queries, int64_t N, int32_t* out_flag) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (n_queries < 0 || N < 1) return fail(SDTW_E_ARG, "N must be >= 1 and n_queries >= 0");
+    if (n_queries == 0) return SDTW_OK;
+    if (n_queries > 0x7fffffff) return fail(SDTW_E_ARG, "n_queries exceeds int32");
+    if (ptr_kind(B) != 1 || ptr_kind(F) != 1 || ptr_kind(out_flag) != 1)
+        return fail(SDTW_E_ARG, "B, F and out_flag must be device pointers on the current device");
+    const cudaStream_t st = g_opt.stream;
+    dominate_kernel<<<(unsigned)n_queries, 256, 0, st>>>(B, F, N, out_flag);
+    CK(cudaGetLastError());
+    g_launches++;
+    CK(cudaStreamSynchronize(st));
+    return SDTW_OK;
+}
+
+sdtw_status sdtw_merge_candidates(const float* cost, const int64_t* end, const int32_t* valid, int64_t n_sets,
+                                  int64_t n_queries, float* out_cost, int64_t* out_end, int32_t* out_invalid) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (n_sets < 1 || n_queries < 0) return fail(SDTW_E_ARG, "n_sets must be >= 1 and n_queries >= 0");
+    if (n_queries == 0) return SDTW_OK;
+    if (ptr_kind(cost) != 1 || ptr_kind(end) != 1 || ptr_kind(out_cost) != 1 || ptr_kind(out_end) != 1 ||
+        (valid && ptr_kind(valid) != 1) || (out_invalid && ptr_kind(out_invalid) != 1))
+        return fail(SDTW_E_ARG, "candidate and output arrays must be device pointers on the current device");
+    const cudaStream_t st = g_opt.stream;
+    merge_kernel<<<(unsigned)((n_queries + 127) / 128), 128, 0, st>>>(cost, end, valid, n_sets, n_queries, out_cost,
+                                                                      out_end, out_invalid);
+    CK(cudaGetLastError());
+    g_launches++;
+    CK(cudaStreamSynchronize(st));
+    return SDTW_OK;
+}
+
+int sdtw_version(void) { return 2; }
+
+#define SDTW_STR2(x) #x
+#define SDTW_STR(x) SDTW_STR2(x)
+const char* sdtw_build_info(void) {
+    return "libsdtw " SDTW_STR(__CUDACC_VER_MAJOR__) "." SDTW_STR(__CUDACC_VER_MINOR__) "." SDTW_STR(
+        __CUDACC_VER_BUILD__) " nvcc/ptxas, sm_100a, float-pair pack mode " SDTW_STR(SDTW_MOV_ASM);
+}
 
 }  // extern "C"

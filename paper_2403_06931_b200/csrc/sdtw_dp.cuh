@@ -112,6 +112,7 @@ struct DpParams {
     // end column, rows [0, N), at col_out[q*N + r] (fp32 cost/end kernels only)
     const float* bnd_user;
     float* col_out;
+    float negzero;         // -0.0f (start-index kernels: the predicated-move FADD operand, never folded)
 };
 
 template <bool TRACE> struct Entry { float d; };
@@ -362,6 +363,29 @@ __device__ __forceinline__ int start_sel(float d, float u, float m, int sd, int 
     return r;
 }
 
+// The same select with the ALU pipe relieved (SDTW_START_PM, default): the ALU pipe (16
+// lanes/clk/SMSP) already carries the FMNMX3 of every cell, and 2 FSETP + 2 SEL made it the
+// bound of the start-index kernel (5 ALU ops per cell).  Here FSETP gives pd = (d == m) and
+// FSETP.AND gives pu = (u == m) && !pd; the result register starts as sd, a PREDICATED FADD
+// (@!pd) overwrites it with sl and a second (@pu) with su -- FMA-pipe moves: x + -0.0 == x
+// bit for bit, denormals kept (no ftz); the int start columns are moved as their float bit
+// patterns, and columns < 2^31 - 2^23 are never NaN patterns.  `nz` is -0.0 from the kernel
+// parameters, so ptxas cannot fold the adds into moves.  ALU: 3 ops per cell instead of 5.
+__device__ __forceinline__ int start_sel_pm(float d, float u, float m, int sd, int su, int sl, float nz) {
+    float r = __int_as_float(sd);
+    asm("{\n\t.reg .pred pu, pd;\n\t"
+        "setp.eq.f32 pd, %1, %3;\n\t"
+        "setp.eq.and.f32 pu, %2, %3, !pd;\n\t"
+        "@!pd add.f32 %0, %5, %6;\n\t"
+        "@pu add.f32 %0, %4, %6;\n\t}"
+        : "+f"(r)
+        : "f"(d), "f"(u), "f"(m), "f"(__int_as_float(su)), "f"(__int_as_float(sl)), "f"(nz));
+    return __float_as_int(r);
+}
+#ifndef SDTW_START_PM
+#define SDTW_START_PM 1
+#endif
+
 // lexicographic (cost, col): "a better than b"
 __device__ __forceinline__ bool better(float ca, int ja, float cb, int jb) {
     return ca < cb || (ca == cb && ja < jb);
@@ -473,6 +497,15 @@ template <int C, int WC, bool TRACE> struct RotRow {
         else return half_of(D[c >> 1][slot(w, off)], orient(c, w, off));
     }
     __device__ __forceinline__ int s_at(int c, int w, int off) const { return S[TRACE ? c : 0][TRACE ? slot(w, off) : 0]; }
+    __device__ __forceinline__ void init(float v) {   // every half of every slot (no partial-pair writes)
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                if constexpr (C == 1) D[p][k] = v;
+                else D[p][k] = pk(v, v);
+            }
+    }
     __device__ __forceinline__ void set_all(int c, float v, int off = 0) {  // every slot of chain c
 #pragma unroll
         for (int w = 0; w < U; ++w) {                           // column w lives in slot(w, off)
@@ -485,6 +518,15 @@ template <int C, int WC> struct Ys {
     static constexpr int NP = (C + 1) / 2;
     using T = typename std::conditional<C == 1, float, unsigned long long>::type;
     T Y[NP][WC];
+    __device__ __forceinline__ void init(float v) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+#pragma unroll
+            for (int w = 0; w < WC; ++w) {
+                if constexpr (C == 1) Y[p][w] = v;
+                else Y[p][w] = pk(v, v);
+            }
+    }
     __device__ __forceinline__ void set(int c, int w, float v) {
         if constexpr (C == 1) Y[0][w] = v;
         else Y[c >> 1][w] = with_half(Y[c >> 1][w], pair_half(c, w), v);
@@ -539,7 +581,7 @@ __device__ __forceinline__ XRow<C> load_xrow_fast(const float* const* xb) {
 // 2x FMNMX3, FFMA2 (2 SASS/cell); the NP pairs are independent within the step.
 template <int C, int WC, bool FMA, bool TRACE, int H>
 __device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, WC>& Y, const XRow<C>& x,
-                                          float lin, int lins, LaneScalars<C>& ls) {
+                                          float lin, int lins, LaneScalars<C>& ls, float nz) {
     using RR = RotRow<C, WC, TRACE>;
     constexpr int NP = RR::NP;
     float left[C], pd[C];
@@ -564,7 +606,8 @@ __device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, W
             if constexpr (TRACE) {
                 const int su = R.S[0][ku];
                 const int sdg = (w == 0) ? psd[0] : R.S[0][kd];
-                const int sv = start_sel(dg, up, m, sdg, su, sl[0]);
+                const int sv = SDTW_START_PM ? start_sel_pm(dg, up, m, sdg, su, sl[0], nz)
+                                             : start_sel(dg, up, m, sdg, su, sl[0]);
                 R.S[0][kd] = sv;
                 sl[0] = sv;
             }
@@ -589,8 +632,10 @@ __device__ __forceinline__ void row_cells(RotRow<C, WC, TRACE>& R, const Ys<C, W
                     const int su0 = R.S[c0][ku], su1 = R.S[c1][ku];
                     const int sd0 = (w == 0) ? psd[c0] : R.S[c0][kd];
                     const int sd1 = (w == 0) ? psd[c1] : R.S[c1][kd];
-                    const int sv0 = start_sel(d0, u0, m0, sd0, su0, sl[c0]);
-                    const int sv1 = start_sel(d1, u1, m1, sd1, su1, sl[c1]);
+                    const int sv0 = SDTW_START_PM ? start_sel_pm(d0, u0, m0, sd0, su0, sl[c0], nz)
+                                                  : start_sel(d0, u0, m0, sd0, su0, sl[c0]);
+                    const int sv1 = SDTW_START_PM ? start_sel_pm(d1, u1, m1, sd1, su1, sl[c1], nz)
+                                                  : start_sel(d1, u1, m1, sd1, su1, sl[c1]);
                     R.S[c0][kd] = sv0;
                     R.S[c1][kd] = sv1;
                     sl[c0] = sv0;
@@ -720,6 +765,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     const int gw = rank * GW + warp;
     const int V = 32 * C * G;
     const int PdMax = P.Pd, K = P.K, RS = P.RS;
+    const float nz = P.negzero;
     const SmemLayout L = smem_layout(C, WC, TRACE, GW, PdMax, RS, XS);
 
     int* pp = reinterpret_cast<int*>(smem + L.off_ctr);        // producer progress seen by warp w
@@ -852,14 +898,15 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     if constexpr (CLUSTER) cluster.sync();
     else __syncthreads();
 
-    // ---- per-lane state
+    // ---- per-lane state.  Whole registers are initialised (both halves of every
+    // pair): set_all / Ys::set re-pack the OTHER half of a pair, and reading an
+    // uninitialised half is undefined (the wrong-cell bug).
     RowT R;
     Ys<C, WC> Y;
+    R.init(INFINITY);
+    Y.init(INFINITY);
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        R.set_all(c, INFINITY);
-#pragma unroll
-        for (int w = 0; w < WC; ++w) Y.set(c, w, INFINITY);
         if constexpr (TRACE) {
 #pragma unroll
             for (int k = 0; k < U; ++k) R.S[c][k] = 0;
@@ -929,7 +976,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                 enter_strip<C, WC, TRACE>(R, Y, c, (long)(pa + pcs[c]) * V + u0 + c, ylane + c * WC, ls, H,
                                           SPEC ? zrow : 0.0f);
         const XRow<C> x = load_xrow<C, XS>(xs, r0, Pd);
-        row_cells<C, WC, FMA, TRACE, H>(R, Y, x, lin, lins, ls);
+        row_cells<C, WC, FMA, TRACE, H>(R, Y, x, lin, lins, ls, nz);
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             if (rcs[c] == N - 1 && pcs[c] >= 0 && pcs[c] < Pl)
@@ -1018,7 +1065,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                             if constexpr (TRACE) lins = e.s;
                         }
                         const XRow<C> x = load_xrow_fast<C, h, XS>(xb);
-                        row_cells<C, WC, FMA, TRACE, h % U>(R, Y, x, lin, lins, ls);
+                        row_cells<C, WC, FMA, TRACE, h % U>(R, Y, x, lin, lins, ls, nz);
                         if (lane == 31) {
                             E o;
                             o.d = ls.right[C - 1];
@@ -1110,7 +1157,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                         if constexpr (TRACE) lins = e.s;
                     }
                     const XRow<C> x = load_xrow_fast<C, h, XS>(xb);
-                    row_cells<C, WC, FMA, TRACE, h % U>(R, Y, x, lin, lins, ls);
+                    row_cells<C, WC, FMA, TRACE, h % U>(R, Y, x, lin, lins, ls, nz);
                     if (lane == 31) {
                         E o;
                         o.d = ls.right[C - 1];

@@ -7,8 +7,12 @@ the per-query records are exchanged with ONE all-gather (NCCL over
 NVLink/NVSwitch on GPUs, gloo in the CPU tests).  The reference is never split:
 a warp path may span any length of it.
 
+Records stay on the communication device: they are packed with tensor views on the GPU
+(no host round trip), gathered, and returned as torch tensors on that device.
 Record layout (int64 x 3 per query): [fp32 cost bits, end, start-or--1]; with the full
 warp path (sdtw_path) a second all-gather moves the per-row column ranges (int32 x 2 x N).
+This module does no arithmetic of the method: the DP, the overtaking test and the
+(cost, end) merges of the reference split all run in the library's kernels.
 """
 from __future__ import annotations
 
@@ -27,25 +31,30 @@ def shard_bounds(Z: int, world: int, rank: int):
     return lo, hi, per
 
 
+def _on(x, dtype, device) -> torch.Tensor:
+    """x (torch tensor or array) as a tensor of `dtype` on `device` (no copy when it is already there)."""
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=dtype)
+    return torch.as_tensor(np.asarray(x), device=device).to(dtype)
+
+
 def _pack(cost, end, start, per: int, device) -> torch.Tensor:
-    cost = torch.as_tensor(np.asarray(cost.cpu() if isinstance(cost, torch.Tensor) else cost, np.float32))
-    end = torch.as_tensor(np.asarray(end.cpu() if isinstance(end, torch.Tensor) else end, np.int64))
-    n = cost.shape[0]
-    rec = torch.full((per, 3), -1, dtype=torch.int64)
+    """[per, 3] int64 records on `device`: fp32 cost bits, end, start (-1 without start)."""
+    rec = torch.full((per, 3), -1, dtype=torch.int64, device=device)
+    n = int(cost.shape[0])
     if n:
-        rec[:n, 0] = cost.view(torch.int32).to(torch.int64)
-        rec[:n, 1] = end
+        rec[:n, 0] = _on(cost, torch.float32, device).view(torch.int32).to(torch.int64)
+        rec[:n, 1] = _on(end, torch.int64, device)
         if start is not None:
-            st = torch.as_tensor(np.asarray(start.cpu() if isinstance(start, torch.Tensor) else start, np.int64))
-            rec[:n, 2] = st
-    return rec.to(device)
+            rec[:n, 2] = _on(start, torch.int64, device)
+    return rec
 
 
 def _unpack(rec: torch.Tensor, Z: int, want_start: bool):
-    rec = rec[:Z].cpu()
-    cost = rec[:, 0].to(torch.int32).view(torch.float32).numpy().copy()
-    end = rec[:, 1].numpy().copy()
-    start = rec[:, 2].numpy().copy() if want_start else None
+    rec = rec[:Z]
+    cost = rec[:, 0].to(torch.int32).view(torch.float32)
+    end = rec[:, 1].clone()
+    start = rec[:, 2].clone() if want_start else None
     return cost, end, start
 
 
@@ -60,6 +69,15 @@ def _gather(t: torch.Tensor, world: int, group):
     return full
 
 
+def comm_device(group=None, device=None):
+    """Where the collectives run: the CUDA device for NCCL, the host for gloo."""
+    if dist.get_backend(group) == "nccl":
+        if device is not None and torch.device(device).type == "cuda":
+            return torch.device(device)
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def distributed_batch(Q, group=None, traceback: bool = False,
                       fn: Optional[Callable] = None, device=None, pre_sharded: bool = False,
                       path: bool = False):
@@ -68,8 +86,9 @@ def distributed_batch(Q, group=None, traceback: bool = False,
     fn(Q_shard) -> (cost, end[, start[, path_lo, path_hi]]); default: this package's CUDA
     ``batch`` / ``traceback`` / ``path``.  With pre_sharded=True, Q is already this rank's
     shard and every rank holds the same number of queries (global Z = world *
-    Q.shape[0]).  Returns numpy (cost[Z], end[Z], start[Z] | None) on every rank, plus
-    (path_lo[Z, N], path_hi[Z, N]) int32 when path=True (a second all-gather)."""
+    Q.shape[0]).  Returns torch tensors on the communication device (the GPU under NCCL,
+    the host under gloo) on every rank: (cost[Z] fp32, end[Z] int64, start[Z] int64 |
+    None), plus (path_lo[Z, N], path_hi[Z, N]) int32 when path=True (a second all-gather)."""
     traceback = traceback or path
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
@@ -85,8 +104,7 @@ def distributed_batch(Q, group=None, traceback: bool = False,
         fn = sd.path if path else (sd.traceback if traceback else sd.batch)
     if device is None:
         device = Q.device if isinstance(Q, torch.Tensor) else torch.device("cpu")
-    if dist.get_backend(group) == "nccl" and device.type != "cuda":
-        device = torch.device("cuda", torch.cuda.current_device())
+    cdev = comm_device(group, device)
     N = int(Q.shape[1]) if len(Q.shape) > 1 else 1
     if hi > lo:
         out = fn(Q[lo:hi])
@@ -94,17 +112,17 @@ def distributed_batch(Q, group=None, traceback: bool = False,
         out = (np.empty(0, np.float32), np.empty(0, np.int64), np.empty(0, np.int64),
                np.empty((0, N), np.int32), np.empty((0, N), np.int32))
     start = out[2] if traceback else None
-    rec = _pack(out[0], out[1], start, per, device)
+    rec = _pack(out[0], out[1], start, per, cdev)
     res = _unpack(_gather(rec, world, group), Z, traceback)
     if not path:
         return res
-    pth = torch.full((per, N, 2), -1, dtype=torch.int32)
+    pth = torch.full((per, N, 2), -1, dtype=torch.int32, device=cdev)
     n = hi - lo
     if n:
-        for k, a in ((0, out[3]), (1, out[4])):
-            pth[:n, :, k] = torch.as_tensor(np.asarray(a.cpu() if isinstance(a, torch.Tensor) else a, np.int32))
-    full = _gather(pth.to(device), world, group)[:Z].cpu().numpy()
-    return res + (full[:, :, 0].copy(), full[:, :, 1].copy())
+        pth[:n, :, 0] = _on(out[3], torch.int32, cdev)
+        pth[:n, :, 1] = _on(out[4], torch.int32, cdev)
+    full = _gather(pth, world, group)[:Z]
+    return res + (full[:, :, 0].contiguous(), full[:, :, 1].contiguous())
 
 
 # --------------------------------------------------------------------------------------
@@ -117,12 +135,17 @@ def distributed_batch(Q, group=None, traceback: bool = False,
 # start) over the first check_cols columns of its slice; where that correction is
 # overtaken by the free DP on every row the result is lexmin(free, correction); queries
 # with a correction not overtaken are recomputed exactly by a rank-ordered chain of full
-# boundary DPs (point-to-point column hand-offs).  The ops object supplies the DP calls
-# (the CUDA library on GPUs; a plain DP in the CPU tests).
+# boundary DPs (point-to-point column hand-offs).  The ops object supplies the DP calls and
+# the two decisions (overtaking test, lexicographic merge): the CUDA library on GPUs, plain
+# numpy in the CPU tests.
 
 
 class CudaSplitOps:
-    """The DP calls of the reference split on the CUDA library (current device)."""
+    """The DP calls and decisions of the reference split on the CUDA library (current device).
+
+    NOTE: set_reference REPLACES this device's library reference with the rank's slice; a
+    later sdtw_batch on this device runs against that slice until set_reference is called
+    again (the library keeps one reference per device)."""
 
     def __init__(self, sd):
         self.sd = sd
@@ -142,11 +165,19 @@ class CudaSplitOps:
         with self.sd.options(OPT_NORMALIZE=0):
             return self.sd.boundary_dp(Q, boundary, free_start=free_start, n_cols=n_cols)
 
+    def columns_dominate(self, B, F):
+        return self.sd.columns_dominate(B, F)
+
+    def merge_candidates(self, cost, end, valid):
+        return self.sd.merge_candidates(cost, end, valid)
+
     def normalize(self, Q, Y):
         """Per-query and whole-reference z-normalisation on the GPU (sdtw_znormalize):
-        the slices must share the global statistics of the reference."""
-        Yd = torch.as_tensor(np.asarray(Y, np.float32), device=Q.device)
-        return self.sd.znormalize(Q), self.sd.znormalize(Yd).cpu().numpy()
+        the slices share the global statistics of the reference.  Exact sums (reading G8) make
+        this bit-identical to set_reference's own grid-reduction normalisation."""
+        Yd = Y.to(device=Q.device, dtype=torch.float32) if isinstance(Y, torch.Tensor) else \
+            torch.as_tensor(np.asarray(Y, np.float32), device=Q.device)
+        return self.sd.znormalize(Q), self.sd.znormalize(Yd)
 
 
 def split_bounds(M: int, world: int, cols: int):
@@ -155,17 +186,19 @@ def split_bounds(M: int, world: int, cols: int):
     return [(min(M, r * per), min(M, (r + 1) * per)) for r in range(world)]
 
 
-def _lexmin(c1, e1, c2, e2):
-    """Element-wise lexicographic min of (cost, end) pairs (numpy)."""
-    take = (c2 < c1) | ((c2 == c1) & (e2 < e1))
-    return np.where(take, c2, c1), np.where(take, e2, e1)
-
-
 def _comm_device(group, dev):
     """gloo moves host tensors (CPU tests, or several ranks sharing one GPU); NCCL device ones."""
     if dist.is_initialized() and dist.get_backend(group) == "gloo":
         return torch.device("cpu")
     return dev
+
+
+def _bits(c) -> torch.Tensor:
+    return c.view(torch.int32).to(torch.int64)
+
+
+def _float(b: torch.Tensor) -> torch.Tensor:
+    return b.to(torch.int32).view(torch.float32)
 
 
 def reference_split_batch(Q: torch.Tensor, Y, ops=None, group=None, normalize: bool = False):
@@ -182,80 +215,71 @@ def reference_split_batch(Q: torch.Tensor, Y, ops=None, group=None, normalize: b
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     Z, N = Q.shape
-    Yn = np.asarray(Y.cpu() if isinstance(Y, torch.Tensor) else Y, np.float32)
-    M = Yn.shape[0]
+    dev = Q.device
+    Yt = _on(Y, torch.float32, dev)
+    M = int(Yt.shape[0])
     cols = ops.round_columns(N)
     bounds = split_bounds(M, world, cols)
     lo, hi = bounds[rank]
     if any(b[1] <= b[0] for b in bounds):
         raise ValueError("reference too short for %d slices of %d-column rounds" % (world, cols))
-    dev = Q.device
     cdev = _comm_device(group, dev)
-    ops.set_reference(torch.as_tensor(Yn[lo:hi], device=dev) if dev.type == "cuda" else Yn[lo:hi])
+    ops.set_reference(Yt[lo:hi].contiguous())
     last = rank < world - 1
     cf, ef, col_check, col_last, check_cols = ops.batch_columns(Q, last)
-    cf = np.asarray(cf.cpu() if isinstance(cf, torch.Tensor) else cf, np.float32)
-    ef = np.asarray(ef.cpu() if isinstance(ef, torch.Tensor) else ef, np.int64) + lo
+    cf = _on(cf, torch.float32, cdev)
+    ef = _on(ef, torch.int64, cdev) + lo
     # 1) every rank's last column -> its successor (one all-gather, Z x N fp32 per rank)
     mine = col_last if col_last is not None else torch.full((Z, N), float("inf"), device=dev)
-    mine = torch.as_tensor(mine, dtype=torch.float32, device=cdev).reshape(Z, N)
-    cols_all = _gather(mine.contiguous(), world, group).reshape(world, Z, N) if world > 1 else mine[None]
-    cols_all = cols_all.to(dev)
-    # 2) correction of this slice from the predecessor's last column
-    cc = np.full(Z, np.inf, np.float32)
-    ec = np.zeros(Z, np.int64)
-    dom = np.ones(Z, bool)
+    mine = _on(mine, torch.float32, cdev).reshape(Z, N).contiguous()
+    cols_all = (_gather(mine, world, group) if world > 1 else mine).reshape(world, Z, N)
+    # 2) correction of this slice from the predecessor's last column (no free start); it is
+    #    usable iff overtaken: its column >= the free DP's column at check_cols - 1, every row
+    cc = torch.full((Z,), float("inf"), dtype=torch.float32, device=cdev)
+    ec = torch.zeros(Z, dtype=torch.int64, device=cdev)
+    dom = torch.ones(Z, dtype=torch.int64, device=cdev)
     if rank > 0:
-        c2, e2, colB = ops.boundary_dp(Q, cols_all[rank - 1], False, check_cols)
-        cc = np.asarray(c2.cpu() if isinstance(c2, torch.Tensor) else c2, np.float32)
-        ec = np.asarray(e2.cpu() if isinstance(e2, torch.Tensor) else e2, np.int64) + lo
-        B = torch.as_tensor(colB, device=dev).reshape(Z, N)
-        F = torch.as_tensor(col_check, device=dev).reshape(Z, N)
-        dom = (B >= F).all(dim=1).cpu().numpy()
-    # 3) per-query records of every rank (one all-gather)
-    rec = torch.zeros((Z, 5), dtype=torch.int64)
-    rec[:, 0] = torch.from_numpy(cf.view(np.int32).astype(np.int64))
-    rec[:, 1] = torch.from_numpy(ef)
-    rec[:, 2] = torch.from_numpy(cc.view(np.int32).astype(np.int64))
-    rec[:, 3] = torch.from_numpy(ec)
-    rec[:, 4] = torch.from_numpy(dom.astype(np.int64))
-    recs = (_gather(rec.to(cdev), world, group).reshape(world, Z, 5) if world > 1 else rec[None]).cpu().numpy()
-    cost = recs[0, :, 0].astype(np.int32).view(np.float32).copy()
-    end = recs[0, :, 1].copy()
-    bad = np.zeros(Z, bool)
-    for r in range(1, world):
-        cost, end = _lexmin(cost, end, recs[r, :, 0].astype(np.int32).view(np.float32), recs[r, :, 1])
-        ok = recs[r, :, 4] != 0
-        cr = np.where(ok, recs[r, :, 2].astype(np.int32).view(np.float32), np.inf).astype(np.float32)
-        cost, end = _lexmin(cost, end, cr, np.where(ok, recs[r, :, 3], 0))
-        bad |= ~ok
-    idx = np.nonzero(bad)[0]
+        c2, e2, colB = ops.boundary_dp(Q, _on(cols_all[rank - 1], torch.float32, dev), False, check_cols)
+        cc = _on(c2, torch.float32, cdev)
+        ec = _on(e2, torch.int64, cdev) + lo
+        dom = _on(ops.columns_dominate(_on(colB, torch.float32, dev).reshape(Z, N),
+                                       _on(col_check, torch.float32, dev).reshape(Z, N)), torch.int64, cdev)
+    # 3) per-query records of every rank (one all-gather): free (cost, end), correction
+    #    (cost, end), overtaken flag
+    rec = torch.stack([_bits(cf), ef, _bits(cc), ec, dom], dim=1)
+    recs = (_gather(rec, world, group) if world > 1 else rec).reshape(world, Z, 5)
+    # lexmin over 2*world candidate sets: every free candidate, every overtaken correction
+    cand_c = torch.cat([_float(recs[:, :, 0]), _float(recs[:, :, 2])], 0)
+    cand_e = torch.cat([recs[:, :, 1], recs[:, :, 3]], 0)
+    valid = torch.cat([torch.ones((world, Z), dtype=torch.int32, device=cdev), recs[:, :, 4].to(torch.int32)], 0)
+    cost, end, bad = ops.merge_candidates(_on(cand_c, torch.float32, dev), _on(cand_e, torch.int64, dev),
+                                          _on(valid, torch.int32, dev))
+    cost = _on(cost, torch.float32, "cpu").numpy().copy()
+    end = _on(end, torch.int64, "cpu").numpy().copy()
+    idx = np.nonzero(_on(bad, torch.int32, "cpu").numpy())[0]
     if idx.size:
         # 4) exact fallback for those queries: rank-ordered chain of full boundary DPs
-        Qf = Q[torch.as_tensor(idx, device=dev)].contiguous()
+        it = torch.as_tensor(idx, device=dev)
+        Qf = Q[it].contiguous()
         F_ = len(idx)
         if rank == 0:
-            tin = None
-            cfl, efl = cf[idx], ef[idx]
-            tout = torch.as_tensor(col_last, device=dev).reshape(Z, N)[torch.as_tensor(idx, device=dev)]
+            cfl, efl = cf[torch.as_tensor(idx, device=cdev)], ef[torch.as_tensor(idx, device=cdev)]
+            tout = _on(col_last, torch.float32, dev).reshape(Z, N)[it]
         else:
             tin = torch.empty((F_, N), dtype=torch.float32, device=cdev)
             dist.recv(tin, src=_global(group, rank - 1), group=group)
-            c3, e3, tout = ops.boundary_dp(Qf, tin.to(dev), True, 0)
-            cfl = np.asarray(c3.cpu() if isinstance(c3, torch.Tensor) else c3, np.float32)
-            efl = np.asarray(e3.cpu() if isinstance(e3, torch.Tensor) else e3, np.int64) + lo
+            c3, e3, tout = ops.boundary_dp(Qf, _on(tin, torch.float32, dev), True, 0)
+            cfl = _on(c3, torch.float32, cdev)
+            efl = _on(e3, torch.int64, cdev) + lo
         if rank < world - 1:
-            dist.send(torch.as_tensor(tout, dtype=torch.float32, device=cdev).reshape(F_, N).contiguous(),
+            dist.send(_on(tout, torch.float32, cdev).reshape(F_, N).contiguous(),
                       dst=_global(group, rank + 1), group=group)
-        rf = torch.zeros((F_, 2), dtype=torch.int64)
-        rf[:, 0] = torch.from_numpy(np.asarray(cfl, np.float32).view(np.int32).astype(np.int64))
-        rf[:, 1] = torch.from_numpy(np.asarray(efl, np.int64))
-        rfs = _gather(rf.to(cdev), world, group).reshape(world, F_, 2).cpu().numpy()
-        c_, e_ = rfs[0, :, 0].astype(np.int32).view(np.float32), rfs[0, :, 1]
-        for r in range(1, world):
-            c_, e_ = _lexmin(c_, e_, rfs[r, :, 0].astype(np.int32).view(np.float32), rfs[r, :, 1])
-        cost[idx], end[idx] = c_, e_
-    end = np.where(np.isinf(cost), 0, end)
+        rf = torch.stack([_bits(cfl), efl], dim=1)
+        rfs = (_gather(rf, world, group) if world > 1 else rf).reshape(world, F_, 2)
+        c_, e_, _ = ops.merge_candidates(_on(_float(rfs[:, :, 0]), torch.float32, dev),
+                                         _on(rfs[:, :, 1], torch.int64, dev), None)
+        cost[idx] = _on(c_, torch.float32, "cpu").numpy()
+        end[idx] = _on(e_, torch.int64, "cpu").numpy()
     return cost.astype(np.float32), end.astype(np.int64), int(idx.size)
 
 

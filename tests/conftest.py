@@ -15,9 +15,14 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
 
-@pytest.fixture(scope="session")
-def brute_lib():
-    """tests/pins/brute.c compiled with gcc (no contraction)."""
+_BRUTE = None
+
+
+def load_brute():
+    """tests/pins/brute.c compiled with gcc (no contraction), loaded once per process."""
+    global _BRUTE
+    if _BRUTE is not None:
+        return _BRUTE
     src = os.path.join(ROOT, "tests", "pins", "brute.c")
     out = os.path.join(ROOT, "tests", "pins", "libbrute.so")
     if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
@@ -33,7 +38,13 @@ def brute_lib():
     L.brute_sdtw.restype = None
     L.restricted_dp.argtypes = [f32p, i64, f32p, i64, ctypes.c_int, i64, i64, f32p, f32p]
     L.restricted_dp.restype = ctypes.c_float
+    _BRUTE = L
     return L
+
+
+@pytest.fixture(scope="session")
+def brute_lib():
+    return load_brute()
 
 
 @pytest.fixture(scope="session")

@@ -57,7 +57,7 @@ def test_library_is_sm100a_native(lib):
 
 def test_version_and_options(lib):
     import paper_2403_06931_b200 as sd
-    assert sd.version() == 1
+    assert sd.version() == 2
     old = sd.get_option(sd.OPT_FMA)
     sd.set_option(sd.OPT_FMA, 0)
     assert sd.get_option(sd.OPT_FMA) == 0

@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, Z, traceback, out_q):
+def _worker(rank, world, port, Z, traceback, out_q):  # noqa: C901
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -37,7 +37,7 @@ def _worker(rank, world, port, Z, traceback, out_q):
             return (r["cost"], r["end"], r["start"]) if traceback else (r["cost"], r["end"])
 
         cost, end, start = distributed_batch(Q, traceback=traceback, fn=fn)
-        out_q.put((rank, cost, end, start))
+        out_q.put((rank, cost.numpy(), end.numpy(), None if start is None else start.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -60,7 +60,7 @@ def _path_worker(rank, world, port, Z, out_q):
                     np.array([r[2] for r in rs], np.int64), np.array([r[3] for r in rs], np.int32),
                     np.array([r[4] for r in rs], np.int32))
 
-        out_q.put((rank,) + distributed_batch(Q, path=True, fn=fn))
+        out_q.put((rank,) + tuple(t.numpy() for t in distributed_batch(Q, path=True, fn=fn)))
     finally:
         dist.destroy_process_group()
 
@@ -88,16 +88,18 @@ def test_gloo_world2_path_matches_single_process(Z):
             assert np.array_equal(lo[k], rlo) and np.array_equal(hi[k], rhi)
 
 
-@pytest.mark.parametrize("Z,traceback", [(7, False), (8, True), (1, True)])
-def test_gloo_world2_matches_single_process(Z, traceback):
+@pytest.mark.parametrize("world,Z,traceback", [(2, 7, False), (2, 8, True), (2, 1, True),
+                                               (3, 7, True), (3, 2, False), (4, 9, True), (4, 3, True)])
+def test_gloo_world_n_matches_single_process(world, Z, traceback):
+    """World sizes 2-4, Z not divisible by the world size, empty shards (Z < world)."""
     import oracle
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, Z, traceback, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, Z, traceback, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in range(2)]
+    res = [q.get(timeout=120) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0

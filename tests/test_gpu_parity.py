@@ -49,6 +49,19 @@ def _inputs(Z, N, M, seed):
     return Q, Y
 
 
+def _restricted(x, Yw, fma, start, end):
+    """D(N-1, end) of the DP allowed to begin only at column `start` (tests/pins/brute.c)."""
+    from tests.conftest import load_brute
+    L = load_brute()
+    f32p = ctypes.POINTER(ctypes.c_float)
+    win = np.ascontiguousarray(Yw[start:end + 1], np.float32)
+    x = np.ascontiguousarray(x, np.float32)
+    a = np.empty(win.shape[0], np.float32)
+    b = np.empty(win.shape[0], np.float32)
+    return np.float32(L.restricted_dp(x.ctypes.data_as(f32p), x.shape[0], win.ctypes.data_as(f32p), win.shape[0],
+                                      int(fma), 0, end - start, a.ctypes.data_as(f32p), b.ctypes.data_as(f32p)))
+
+
 def _check_exact(Q, Y, got, fma=True, trace=False, ref=None):
     c, e, s = got
     if ref is None:
@@ -61,6 +74,11 @@ def _check_exact(Q, Y, got, fma=True, trace=False, ref=None):
     if trace:
         same = e == ref["end"]
         assert np.array_equal(s[same], ref["start"][same])
+        Q2 = np.atleast_2d(Q)
+        for q in bad:  # a tied end: its start must still be valid (restricted DP reaches the cost)
+            if np.isfinite(c[q]):
+                assert 0 <= s[q] <= e[q], (q, s[q], e[q])
+                assert _restricted(Q2[q], Y, fma, int(s[q]), int(e[q])) == c[q], (q, s[q], e[q])
     return ref
 
 
@@ -165,30 +183,30 @@ def test_host_pointers_match_device_pointers():
 
 
 # --------------------------------------------------------------- normaliser
-def test_znormalize_matches_oracle():
-    Q = nanopore_queries(64, 2000, 50000, 21)
+@pytest.mark.parametrize("Z,L", [(64, 2000), (7, 1), (5, 3), (3, 4097), (2, 100_000)])
+def test_znormalize_matches_oracle(Z, L):
+    """Reading G8: exact sums on both sides -> the normaliser is bit-exact (0 mismatches)."""
+    Q = nanopore_queries(Z, L, max(L, 50000), 21) if L >= 64 else \
+        np.random.default_rng(L).standard_normal((Z, L)).astype(np.float32) * 12 + 90
     z = sd.znormalize(torch.as_tensor(Q, device=DEV)).cpu().numpy()
     zo = oracle.znorm(Q)
-    diff = np.abs(z.astype(np.float64) - zo)
-    assert np.count_nonzero(diff) <= 64            # summation order may flip a last bit
-    assert diff.max() <= 2.4e-7
+    assert np.array_equal(z.view(np.uint32), zo.view(np.uint32)), np.count_nonzero(z != zo)
     zc = sd.znormalize(np.full((2, 10), 7.0, np.float32))
     assert np.all(zc == 0)
 
 
-def test_normalized_end_to_end_tolerance():
+def test_normalized_end_to_end_bit_exact():
+    """Normalisation inside the call (reference at set_reference, queries per batch) equals
+    the oracle's normaliser followed by the oracle's DP, bit for bit (reading G8)."""
     Yraw = nanopore_reference(50_000, 4)
     Qraw = nanopore_queries(32, 1000, 50_000, 4)
     with sd.options(OPT_NORMALIZE=1):
         sd.set_reference(torch.as_tensor(Yraw, device=DEV))
         c, e = sd.batch(torch.as_tensor(Qraw, device=DEV))
     c, e = c.cpu().numpy(), e.cpu().numpy()
-    ref = oracle.sdtw_normalized(Qraw, Yraw)
-    assert np.all(np.abs(c - ref["cost"]) <= 1e-5 * ref["cost"])
     Yn = oracle.znorm(Yraw[None])[0]
-    lr = oracle.sdtw(oracle.znorm(Qraw), Yn, last_rows=True)["last_rows"]
-    for q in np.nonzero(e != ref["end"])[0]:
-        assert lr[q, e[q]] <= ref["cost"][q] * (1 + 1e-5)
+    Qn = oracle.znorm(Qraw)
+    _check_exact(Qn, Yn, (c, e, None))
 
 
 # --------------------------------------------------------------- errors

@@ -301,6 +301,40 @@ def test_normalizer_stats_recheck(oracle_mod):
     assert np.max(np.abs(ref.astype(np.float64) - Z)) <= 2.4e-7
 
 
+def test_normalizer_exact_sums_order_free(oracle_mod):
+    """Reading G8: the sums are exact, rounded once, so (a) permuting a
+    series permutes z bit for bit -- a plain sequential fp64 accumulation fails this on
+    most of these series (checked below, so the pin discriminates) -- and (b) z equals the
+    value computed from EXACT RATIONAL sums (fractions.Fraction, rounded once to fp64 by
+    float()), independently of math.fsum."""
+    from fractions import Fraction
+    from datagen import nanopore_queries
+    Q = nanopore_queries(24, 2000, 50000, 23)
+    rng = np.random.default_rng(23)
+    perm = rng.permutation(Q.shape[1])
+    z = oracle_mod.znorm(Q)
+    zp = oracle_mod.znorm(Q[:, perm])
+    assert np.array_equal(zp.view(np.uint32), z[:, perm].view(np.uint32))
+    naive_differs = 0
+    for q in range(Q.shape[0]):
+        a = b = 0.0
+        for v, w in zip(Q[q].astype(np.float64), Q[q, perm].astype(np.float64)):
+            a += v * v
+            b += w * w
+        naive_differs += a != b
+    assert naive_differs >= 4
+    for q in range(4):
+        x = Q[q].astype(np.float64)
+        n = x.shape[0]
+        s = float(sum(Fraction(v) for v in x))
+        s2 = float(sum(Fraction(v) * Fraction(v) for v in x))
+        mean = s / n
+        ex2 = s2 / n
+        sd = np.sqrt(ex2 - mean * mean)
+        ref = ((x - mean) / sd).astype(np.float32)
+        assert np.array_equal(ref.view(np.uint32), z[q].view(np.uint32)), q
+
+
 def test_normalizer_affine_invariance(oracle_mod):
     rng = np.random.default_rng(22)
     x = rng.standard_normal((10, 777)).astype(np.float32)

@@ -72,6 +72,22 @@ class NumpyOps:
             c.append(b[0]); e.append(b[1]); col.append(cols[-1])
         return np.array(c, F32), np.array(e, np.int64), torch.tensor(np.array(col))
 
+    # the two decisions (the CUDA library's sdtw_columns_dominate / sdtw_merge_candidates)
+    def columns_dominate(self, B, F):
+        return torch.tensor((np.asarray(B) >= np.asarray(F)).all(axis=1).astype(np.int32))
+
+    def merge_candidates(self, cost, end, valid):
+        c, e = np.asarray(cost), np.asarray(end)
+        v = np.ones(c.shape, bool) if valid is None else np.asarray(valid) != 0
+        bc = np.full(c.shape[1], INF)
+        be = np.zeros(c.shape[1], np.int64)
+        for k in range(c.shape[0]):
+            take = v[k] & ((c[k] < bc) | ((c[k] == bc) & (e[k] < be)))
+            bc = np.where(take, c[k], bc)
+            be = np.where(take, e[k], be)
+        be = np.where(np.isinf(bc), 0, be)
+        return torch.tensor(bc), torch.tensor(be), torch.tensor((~v).any(axis=0).astype(np.int32))
+
 
 def _free_port():
     s = socket.socket()
