@@ -4,7 +4,7 @@ into profiles/issue_<config>.json (read by bench.py: roofline.issue_slots_per_ce
     python scripts/ncu_issue.py <report.ncu-rep> <config> <Z> <N> <M> [precision]
 
 issue slots per cell   = smsp__inst_executed.sum * 32 / (Z*N*M)   (warp instructions x lanes)
-thread inst per cell   = smsp__thread_inst_executed.sum / (Z*N*M) (active lanes only)
+thread inst per cell   = sass__thread_inst_executed_true_per_opcode / (Z*N*M) (predicated-on lanes)
 issue_active           = smsp__issue_active.avg.pct_of_peak_sustained_active / 100
 """
 import csv
@@ -41,7 +41,9 @@ def main():
     rows = [d for d in raw_metrics(rep) if "sdtw_dp" in d.get("Kernel Name", ("", ""))[0]]
     d = rows[-1]
     warp = num(d, "smsp__inst_executed.sum")
-    thread = num(d, "smsp__thread_inst_executed.sum")
+    key = "smsp__thread_inst_executed.sum" if "smsp__thread_inst_executed.sum" in d else \
+        "sass__thread_inst_executed_true_per_opcode"
+    thread = num(d, key)
     act = float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"][0].replace(",", "")) / 100.0
     out = {"config": config, "Z": int(Z), "N": int(N), "M": int(M), "precision": prec,
            "warp_inst": warp, "thread_inst": thread, "cells": cells,
