@@ -358,8 +358,12 @@ def main():
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     popt = sd.get_option(sd.OPT_PACKED)
-    packed = popt > 0 or (popt < 0 and not trace)          # the library's auto choice (sdtw_api.cu plan)
-    mix = "half2" if args.half else ("packed" if packed else "scalar") + "_fma" + ("_trace" if trace else "")
+    # the library's auto choice (sdtw_api.cu plan): packed chains for cost/end and for the
+    # checkpointed start index (OPT_START 0/2: the cost/end kernel + window walk-back)
+    ckpt_start = trace and sd.get_option(sd.OPT_START) != 1 and popt in (-1, 1)
+    packed = popt > 0 or (popt < 0 and (not trace or ckpt_start))
+    mix = "half2" if args.half else ("packed" if packed else "scalar") + "_fma" + (
+        "_trace" if trace and not ckpt_start else "")
     k = SASS_PER_CELL[mix]
     peak = sms * LANES_PER_SM * fmax * 1e6 / k / 1e9
     peak3 = sms * LANES_PER_SM * fmax * 1e6 / 3.0 / 1e9
@@ -376,7 +380,11 @@ def main():
     meas = _issue_counts(args.config, w, 16 if args.half else 32)
     if meas:
         roof.update(meas)
-    if trace:
+    if ckpt_start:
+        roof["start_index"] = ("checkpointed (DESIGN.md §15): cost/end DP kernel with round checkpoints, "
+                               "then window DP + walk-back; DP kernel %.1f ms of a %.1f ms step"
+                               % (dp_avg, tot_ms / args.steps))
+    elif trace:
         # the start-index cell needs 5 ALU-pipe ops (FMNMX3 + 2 FSETP + 2 SEL; the ALU pipe
         # issues 16 lanes/clk/SMSP): that pipe, not issue, binds it (ncu: alu 72 % busy)
         alu_peak = sms * 64 * fmax * 1e6 / 5.0 / 1e9

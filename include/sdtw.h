@@ -70,6 +70,15 @@ enum {
     SDTW_OPT_WORKERS = 13,  /* resident CTAs per SM under persistent scheduling; 0 = auto
                                (min(occupancy, n_queries / #SMs)) */
     SDTW_OPT_PAD = 15,      /* extra idle rows per round period (ring slack for long rings); 0 = auto */
+    SDTW_OPT_START = 17,    /* how sdtw_traceback / sdtw_path find the start column: 0 (default)
+                               auto = checkpointed when the launch qualifies, else forward;
+                               1 forward propagation of the start column in every cell
+                               (DESIGN.md §4 TRACE); 2 checkpointed only (SDTW_E_ARG if the
+                               launch does not qualify): the cost/end DP at full speed storing
+                               every round's last column, then per query a window DP from the
+                               checkpoint left of its end and the paper's walk-back,
+                               widened until the chain starts inside.  Both
+                               give the same start (reading G6) */
     SDTW_OPT_SPEC_ROUNDS = 16, /* speculative segments: rounds of each correction pass (the
                                columns over which the boundary's paths must be overtaken by
                                the segment's own); 0 = auto (>= 3 query lengths).  A segment

@@ -11,6 +11,7 @@
 #include "sdtw_dp16.cuh"
 #include "sdtw_path.cuh"
 #include "sdtw_prep.cuh"
+#include "sdtw_start.cuh"
 
 #include <atomic>
 #include <cstdio>
@@ -41,6 +42,7 @@ struct Options {
     int precision = 32;  // 32 fp32 cells; 16 packed half (sdtw_dp16.cuh)
     int pad = 0;         // extra idle rows per round period (0 = auto)
     int spec_rounds = 0; // speculative segments: rounds per correction pass (0 = auto)
+    int start = 0;       // start index: 0 auto, 1 forward propagation, 2 checkpoints + walk-back
     cudaStream_t stream = 0;
 };
 Options g_opt;
@@ -63,6 +65,13 @@ struct Ctx {
     int* order_d = nullptr; size_t order_n = 0;     // unit grab order (device) and its key
     int4* utab_d = nullptr; size_t utab_n = 0;      // speculative segments: unit-kind table
     float* ws_fix = nullptr; size_t ws_fix_n = 0;   // speculative segments: recomputed queries
+    float* ws_fixck = nullptr; size_t ws_fixck_n = 0;   // their round checkpoints
+    float* ws_ck = nullptr; size_t ws_ck_n = 0;     // round checkpoints [Z][Pr][Pd] (checkpointed start index)
+    float* ws_ckc = nullptr; size_t ws_ckc_n = 0;   // speculative correction units' checkpoints
+    unsigned char* ws_win = nullptr; size_t ws_win_n = 0;   // start windows: codes, rows, query lists
+    unsigned char* ws_start = nullptr; size_t ws_start_n = 0;   // start windows: starts (+ paths)
+    double last_win_ms = 0.0;                       // checkpointed start index: window phase time
+    int last_start_iters = 0;                       // ... and its window-widening iterations
     int64_t last_fixups = 0;                        // queries recomputed by the last call
     int64_t order_key[3] = {-1, -1, -1};
     int* flag_d = nullptr;
@@ -161,6 +170,7 @@ struct LaunchCfg {
     int xs;          // single-row query layout (long queries)
     int spec = 0;    // speculative segments: Sseg segments, correction passes of Rc rounds
     int Sseg = 0, Rc = 0;
+    int ck = 0;      // round checkpoints (the CKPT kernel)
 };
 
 // Ragged batch descriptor (host): offsets[Z+1], the longest and shortest query.
@@ -340,7 +350,9 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
 }
 
 sdtw_status launch_dp(const LaunchCfg& c, bool fma, bool trace, const DpParams& p, cudaStream_t st) {
-    DpKernel k = pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0, c.half != 0, c.xs != 0);
+    DpKernel k = c.ck ? sdtw::pick_dp_c2ck(c.WC, fma, c.xs != 0)
+                      : pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0, c.half != 0, c.xs != 0);
+    if (!k) return fail(SDTW_E_ARG, "no kernel for this configuration");
     CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem));
     if (c.CL > 8) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t lc;
@@ -449,6 +461,8 @@ struct SegReq {
     int free_start = 1;            // mode 2: 0 = virtual row -1 is +inf
     int64_t cols = 0;              // mode 2: reference columns to run (multiple of the round width; 0 = all)
     float* col_out = nullptr;      // mode 2: end column [Z][N] (device) or nullptr
+    float* ck = nullptr;           // mode 3: round checkpoints [Z][Pr][Pd] (device), exact after the call
+    int ck_Pr = 0, ck_Pd = 0;      // mode 3: the layout the caller allocated (must match the plan)
 };
 
 sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
@@ -460,7 +474,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
 // their results replace the speculative ones.
 sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const std::vector<int64_t>* off,
                        const int* fix_d, float* dc, int64_t* de, int64_t* ds, cudaStream_t st,
-                       float* col_last = nullptr) {
+                       float* col_last = nullptr, const SegReq* ckr = nullptr) {
     std::vector<int> fix((size_t)Z);
     CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(fix.data(), fix_d, (size_t)Z * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -504,7 +518,21 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
     g_opt.stream = st;
     const int64_t fixed_before = F;
     float* fcol = rows + off2[F];
-    if (col_last) {                                   // also the true last column: one-unit DP per query
+    float* fck = nullptr;
+    if (ckr) {                                        // round checkpoints of the recomputed queries
+        const size_t per = (size_t)ckr->ck_Pr * ckr->ck_Pd;
+        s = grow(&ctx->ws_fixck, &ctx->ws_fixck_n, (size_t)F * per);
+        if (s == SDTW_OK) {
+            fck = ctx->ws_fixck;
+            SegReq r3 = *ckr;
+            r3.ck = fck;
+            s = run_batch(rows, F, N, fc, fe, nullptr, false, nullptr, Ragged(), &r3);
+        }
+        if (s == SDTW_OK)
+            for (int64_t k = 0; k < F; ++k)
+                CK(cudaMemcpyAsync(ckr->ck + idx[k] * per, fck + k * per, per * sizeof(float), cudaMemcpyDeviceToDevice,
+                                   st));
+    } else if (col_last) {                            // also the true last column: one-unit DP per query
         g_opt.sched = 3;
         SegReq r2;
         r2.mode = 2;
@@ -617,7 +645,14 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     if (s != SDTW_OK) return s;
     if (rg.off && cfg.dual) return fail(SDTW_E_ARG, "ragged batches need OPT_PACKED in {0, 1, 2}");
     const int smode = sr ? sr->mode : 0;
-    if (smode) {
+    if (smode == 3) {                                   // round checkpoints
+        if (trace || rg.off || cfg.half || cfg.dual || cfg.CL != 1 || cfg.C != 2 || !sdtw::pick_dp_c2ck(cfg.WC, true, false))
+            return fail(SDTW_E_ARG, "round checkpoints need the two-chain fp32 cost/end kernel (no clusters, "
+                                    "fixed-length queries)");
+        if (cfg.Pr != sr->ck_Pr || cfg.Pd != sr->ck_Pd)
+            return fail(SDTW_E_CUDA, "internal: checkpoint layout does not match the launch plan");
+        cfg.ck = 1;
+    } else if (smode) {
         if (!cfg.spec || trace || rg.off || cfg.half)
             return fail(SDTW_E_ARG, "reference-split calls need fp32 cost/end, fixed-length queries and the "
                                     "speculative schedule (no clusters, OPT_SCHED 0 or 3, >= 4(Rc+1) rounds)");
@@ -724,6 +759,20 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.bnd_user = nullptr;
     p.col_out = nullptr;
     p.negzero = -0.0f;
+    p.ckpt = nullptr;
+    p.ckpt_c = nullptr;
+    p.ck_sg = 0;
+    p.ck_rc = 0;
+    if (cfg.ck) {
+        p.ckpt = sr->ck;
+        if (cfg.spec && cfg.Sseg > 1) {
+            s = grow(&ctx->ws_ckc, &ctx->ws_ckc_n, (size_t)Z * (cfg.Sseg - 1) * cfg.Rc * cfg.Pd);
+            if (s != SDTW_OK) return s;
+            p.ckpt_c = ctx->ws_ckc;
+        }
+        p.ck_sg = cfg.Sseg;
+        p.ck_rc = cfg.Rc;
+    }
     int* fix_d = nullptr;
     ctx->last_fixups = 0;
     if (cfg.persistent) {
@@ -820,8 +869,14 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
                                      (size_t)N * 4, (size_t)Z, cudaMemcpyDeviceToDevice, st));
             if (sr->check_cols) *sr->check_cols = (int64_t)cfg.Rc * 32LL * cfg.C * cfg.GW * cfg.WC;
         }
+        if (cfg.ck && cfg.Sseg > 1) {                       // exact columns inside the correction rounds
+            sdtw::merge_ckpt_kernel<<<dim3((unsigned)(cfg.Sseg - 1), (unsigned)Z), 256, 0, st>>>(
+                p.ckpt, p.ckpt_c, fix_d, cfg.Pr, cfg.Pd, (int)N, cfg.Sseg, cfg.Rc);
+            CK(cudaGetLastError());
+            g_launches++;
+        }
         s = spec_fixup(ctx, xd, Z, N, rg.off, fix_d, dc, de, trace ? ds : nullptr, st,
-                       smode == 1 ? sr->col_last : nullptr);
+                       smode == 1 ? sr->col_last : nullptr, cfg.ck ? sr : nullptr);
         if (s != SDTW_OK) return s;
     } else if (cfg.persistent) {
         sdtw::finalize_kernel<<<(unsigned)((Z + 127) / 128), 128, 0, st>>>(
@@ -855,6 +910,185 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         if (trace && ds != out_start) CK(cp(out_start, ds, Z * sizeof(int64_t), ks));
         CK(cudaStreamSynchronize(st));
     }
+    return SDTW_OK;
+}
+
+// Checkpointed start index: the cost/end DP with round checkpoints at the
+// full cost/end speed, then per query a window DP from the checkpoint left of its end and
+// the walk-back (sdtw_start.cuh), widening the window for the few queries whose chain
+// starts further left.  Returns SDTW_E_ARG (before touching any output) when the launch
+// does not qualify, so that the caller can fall back to forward propagation.
+constexpr size_t kWinBudget = size_t(8) << 30;   // codes of one launch (all queries of a batch, normally)
+
+sdtw_status run_traceback_ckpt(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
+                               int64_t* out_start, int32_t* path_lo = nullptr, int32_t* path_hi = nullptr) {
+    if (N < 1 || Z < 0) return fail(SDTW_E_ARG, "N must be >= 1 and n_queries >= 0");
+    if (Z > 0 && (!Q || !out_cost || !out_end || !out_start)) return fail(SDTW_E_ARG, "NULL pointer");
+    if (Z > 0x7fffffff || N > 0x7fffffff) return fail(SDTW_E_ARG, "sizes exceed int32");
+    Ctx* ctx;
+    sdtw_status s = get_ctx(&ctx);
+    if (s != SDTW_OK) return s;
+    if (!ctx->ref) return fail(SDTW_E_NOREF, "no reference set on this device");
+    if (Z == 0) return run_batch(Q, 0, N, out_cost, out_end, out_start, true);
+    if (ctx->M >= (1LL << 31) - (1LL << 23)) return fail(SDTW_E_ARG, "reference too long for checkpoints");
+    LaunchCfg cfg;
+    s = plan(*ctx, Z, N, false, &cfg);
+    if (s != SDTW_OK) return s;
+    if (cfg.half || cfg.dual || cfg.CL != 1 || cfg.C != 2 || !sdtw::pick_dp_c2ck(cfg.WC, true, false))
+        return fail(SDTW_E_ARG, "checkpointed start index needs the two-chain fp32 cost/end kernel");
+    const size_t per = (size_t)cfg.Pr * cfg.Pd;
+    const size_t ck_bytes = (size_t)Z * per * sizeof(float);
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); free_b = 0; }
+    const size_t have_b = ctx->ws_ck_n * sizeof(float);
+    if (ck_bytes > have_b && ck_bytes > (free_b + have_b) / 2)
+        return fail(SDTW_E_ARG, "round checkpoints exceed half the free device memory");
+    s = grow(&ctx->ws_ck, &ctx->ws_ck_n, (size_t)Z * per);
+    if (s != SDTW_OK) return s;
+    const int64_t launches0 = g_launches.load();
+    // 1) cost/end with round checkpoints (device-side results in bd)
+    SegReq r;
+    r.mode = 3;
+    r.ck = ctx->ws_ck;
+    r.ck_Pr = cfg.Pr;
+    r.ck_Pd = cfg.Pd;
+    BatchDev bd;
+    const Options o = g_opt;
+    cudaStream_t st = o.stream;
+    float ms_dp = 0.0f;
+    s = run_batch(Q, Z, N, out_cost, out_end, nullptr, false, &bd, Ragged(), &r);
+    if (s != SDTW_OK) return s;
+    ms_dp = (float)ctx->last_dp_ms;
+    const int ks = ptr_kind(out_start);
+    const int kl = path_lo ? ptr_kind(path_lo) : 1, kh = path_hi ? ptr_kind(path_hi) : 1;
+    if (ks < 0 || kl < 0 || kh < 0) return fail(SDTW_E_ARG, "device pointer on another device");
+    if (o.profile) CK(cudaEventRecord(ctx->ev0, st));
+    // 2) windows: per query the round of its end and the previous one first
+    std::vector<int64_t> he(Z);
+    std::vector<float> hc(Z);
+    CK(cudaMemcpyAsync(he.data(), bd.end, Z * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc.data(), bd.cost, Z * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t cpr = 32LL * cfg.C * cfg.GW * cfg.WC;
+    const bool want_path = path_lo != nullptr;
+    // results: start [Z] (+ path [Z][N] x 2), kept across iterations; the per-launch scratch
+    // (query lists, codes, row buffers) lives in ws_win and may grow between launches
+    const size_t fixed = (size_t)Z * 8 + (want_path ? (size_t)Z * N * 8 : 0);
+    if (fixed > ctx->ws_start_n) {
+        if (ctx->ws_start) cudaFree(ctx->ws_start);
+        ctx->ws_start = nullptr;
+        ctx->ws_start_n = 0;
+        CK(cudaMalloc(&ctx->ws_start, fixed));
+        ctx->ws_start_n = fixed;
+    }
+    int64_t* ds = reinterpret_cast<int64_t*>(ctx->ws_start);
+    int32_t* dlo = want_path ? reinterpret_cast<int32_t*>(ds + Z) : nullptr;
+    int32_t* dhi = want_path ? dlo + (size_t)Z * N : nullptr;
+    std::vector<int> act, k0(Z, 0), kend(Z, 0);
+    for (int64_t q = 0; q < Z; ++q) {
+        kend[q] = (int)(he[q] / cpr);
+        k0[q] = kend[q];                     // the end's own round first (most chains start in it)
+        act.push_back((int)q);               // +inf costs: the walk writes start 0 (and -1 paths)
+    }
+    std::vector<int64_t> hs(Z, -1);
+    int iters = 0;
+    while (!act.empty()) {
+        if (++iters > 64) return fail(SDTW_E_CUDA, "internal: start windows did not converge");
+        // chunks of queries whose codes fit the budget
+        size_t pos = 0;
+        while (pos < act.size()) {
+            int64_t Lmax = 1;
+            size_t n = 0;
+            size_t bytes = 0;
+            while (pos + n < act.size()) {
+                const int q = act[pos + n];
+                const int64_t L = std::max<int64_t>(1, he[q] - (int64_t)k0[q] * cpr + 1);
+                const int64_t Lm = std::max(Lmax, L);
+                const size_t W = (size_t)((Lm + 15) / 16);
+                const size_t b = (n + 1) * ((size_t)N * W * 4 + (size_t)Lm * 4 + 8);
+                if (n > 0 && b > kWinBudget) break;
+                Lmax = Lm;
+                bytes = b;
+                ++n;
+            }
+            const int W = (int)((Lmax + 15) / 16);
+            const size_t need = bytes + 256;
+            if (need > ctx->ws_win_n) {
+                CK(cudaStreamSynchronize(st));                 // earlier launches may still read it
+                if (ctx->ws_win) cudaFree(ctx->ws_win);
+                ctx->ws_win = nullptr;
+                ctx->ws_win_n = 0;
+                CK(cudaMalloc(&ctx->ws_win, need));
+                ctx->ws_win_n = need;
+            }
+            unsigned char* b0 = ctx->ws_win;
+            int* dq = reinterpret_cast<int*>(b0);
+            int* dk = dq + n;
+            uint32_t* codes = reinterpret_cast<uint32_t*>(((uintptr_t)(dk + n) + 15) & ~(uintptr_t)15);
+            float* rowbuf = reinterpret_cast<float*>(codes + n * (size_t)N * W);
+            std::vector<int> lists(2 * n);
+            for (size_t t = 0; t < n; ++t) { lists[t] = act[pos + t]; lists[n + t] = k0[act[pos + t]]; }
+            CK(cudaMemcpyAsync(dq, lists.data(), 2 * n * sizeof(int), cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));                     // `lists` is pageable host memory
+            sdtw::WinParams wp;
+            wp.X = bd.x;
+            wp.Y = ctx->ref;
+            wp.cost = bd.cost;
+            wp.end = bd.end;
+            wp.ck = ctx->ws_ck;
+            wp.qidx = dq;
+            wp.k0 = dk;
+            wp.cpr = cpr;
+            wp.Pr = cfg.Pr;
+            wp.Pd = cfg.Pd;
+            wp.N = (int)N;
+            wp.W = W;
+            wp.Lmax = (int)Lmax;
+            wp.codes = codes;
+            wp.rowbuf = rowbuf;
+            wp.out_start = ds;
+            wp.path_lo = dlo;
+            wp.path_hi = dhi;
+            wp.err_flag = ctx->flag_d;
+            const int T = (int)std::min<int64_t>(256, (N + 31) / 32 * 32);
+            if (o.fma) sdtw::window_dp_kernel<true><<<(unsigned)n, T, 2 * T * sizeof(float), st>>>(wp);
+            else sdtw::window_dp_kernel<false><<<(unsigned)n, T, 2 * T * sizeof(float), st>>>(wp);
+            sdtw::window_walk_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(wp, (int)n);
+            CK(cudaGetLastError());
+            g_launches += 2;
+            pos += n;
+        }
+        CK(cudaMemcpyAsync(hs.data(), ds, Z * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (*ctx->flag_h) return fail(SDTW_E_CUDA, "internal: window recomputation did not reproduce the batch cost");
+        std::vector<int> next;
+        for (int q : act)
+            if (hs[q] < 0) {                                  // the chain leaves the window: double it
+                const int width = kend[q] - k0[q] + 1;
+                k0[q] = std::max(0, k0[q] - width);
+                next.push_back(q);
+            }
+        act.swap(next);
+    }
+    if (o.profile) {
+        float ms = 0.f;
+        CK(cudaEventRecord(ctx->ev1, st));
+        CK(cudaEventSynchronize(ctx->ev1));
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        ctx->last_dp_ms = ms_dp;                          // the DP kernel alone
+        ctx->last_win_ms = ms;
+    }
+    // 3) outputs: the starts (and paths) wherever they live
+    CK(cudaMemcpyAsync(out_start, ds, Z * sizeof(int64_t), ks ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (want_path) {
+        CK(cudaMemcpyAsync(path_lo, dlo, (size_t)Z * N * 4, kl ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(path_hi, dlo + (size_t)Z * N, (size_t)Z * N * 4,
+                           kh ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    ctx->last_launches = g_launches.load() - launches0;
+    ctx->last_start_iters = iters;
     return SDTW_OK;
 }
 
@@ -1068,6 +1302,12 @@ sdtw_status sdtw_round_columns(int64_t N, int64_t* cols) {
 sdtw_status sdtw_traceback(const float* Q, int64_t n_queries, int64_t N, float* out_cost, int64_t* out_end,
                            int64_t* out_start) {
     std::lock_guard<std::mutex> lk(g_mu);
+    if (g_opt.start != 1) {
+        // checkpointed start index; SDTW_E_ARG from it means "does not qualify" (no output
+        // written yet) -- fall back to forward propagation unless it was forced
+        const sdtw_status s = run_traceback_ckpt(Q, n_queries, N, out_cost, out_end, out_start);
+        if (s != SDTW_E_ARG || g_opt.start == 2) return s;
+    }
     return run_batch(Q, n_queries, N, out_cost, out_end, out_start, true);
 }
 
@@ -1105,6 +1345,11 @@ sdtw_status sdtw_batch_ragged(const float* Q, const int64_t* offsets, int64_t n_
 sdtw_status sdtw_path(const float* Q, int64_t n_queries, int64_t N, float* out_cost, int64_t* out_end,
                       int64_t* out_start, int32_t* path_lo, int32_t* path_hi) {
     std::lock_guard<std::mutex> lk(g_mu);
+    if (g_opt.start != 1 && n_queries > 0 && path_lo && path_hi) {
+        // the checkpointed start's walk-back IS the warp path (same window, same codes)
+        const sdtw_status s = run_traceback_ckpt(Q, n_queries, N, out_cost, out_end, out_start, path_lo, path_hi);
+        if (s != SDTW_E_ARG || g_opt.start == 2) return s;
+    }
     return run_path(Q, n_queries, N, out_cost, out_end, out_start, path_lo, path_hi);
 }
 
@@ -1172,6 +1417,7 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_PRECISION: if (v != 16 && v != 32) break; g_opt.precision = (int)v; return SDTW_OK;
         case SDTW_OPT_PAD: if (v < 0 || v > (1 << 20)) break; g_opt.pad = (int)v; return SDTW_OK;
         case SDTW_OPT_SPEC_ROUNDS: if (v < 0 || v > 4096) break; g_opt.spec_rounds = (int)v; return SDTW_OK;
+        case SDTW_OPT_START: if (v < 0 || v > 2) break; g_opt.start = (int)v; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
     return fail(SDTW_E_ARG, "bad value for option " + std::to_string(key));
@@ -1197,6 +1443,7 @@ sdtw_status sdtw_get_option(int key, int64_t* v) {
         case SDTW_OPT_PRECISION: *v = g_opt.precision; return SDTW_OK;
         case SDTW_OPT_PAD: *v = g_opt.pad; return SDTW_OK;
         case SDTW_OPT_SPEC_ROUNDS: *v = g_opt.spec_rounds; return SDTW_OK;
+        case SDTW_OPT_START: *v = g_opt.start; return SDTW_OK;
         default: return fail(SDTW_E_ARG, "unknown option key " + std::to_string(key));
     }
 }
@@ -1243,6 +1490,11 @@ void sdtw_release(void) {
     cudaFree(c.order_d);
     cudaFree(c.utab_d);
     cudaFree(c.ws_fix);
+    cudaFree(c.ws_fixck);
+    cudaFree(c.ws_ck);
+    cudaFree(c.ws_ckc);
+    cudaFree(c.ws_win);
+    cudaFree(c.ws_start);
     cudaFree(c.flag_d);
     cudaFreeHost(c.flag_h);
     cudaEventDestroy(c.ev0);

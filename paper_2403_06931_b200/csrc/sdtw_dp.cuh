@@ -113,6 +113,14 @@ struct DpParams {
     const float* bnd_user;
     float* col_out;
     float negzero;         // -0.0f (start-index kernels: the predicated-move FADD operand, never folded)
+    // round checkpoints (CKPT kernels): the last column of every round as the
+    // unit computed it, rows [0, Pd), at ckpt[(q*Pr + p)*Pd + r] for the free-DP units (A_s,
+    // B_s, sequential segments, one CTA per ring) and at ckpt_c[((q*(Sg-1) + s-1)*Rc + j)*Pd
+    // + r] for the correction units C_s (their j-th round); merged into the true column
+    // min(free, correction) by merge_ckpt_kernel.
+    float* ckpt;
+    float* ckpt_c;
+    int ck_sg, ck_rc;
 };
 
 template <bool TRACE> struct Entry { float d; };
@@ -383,7 +391,7 @@ __device__ __forceinline__ int start_sel_pm(float d, float u, float m, int sd, i
     return __float_as_int(r);
 }
 #ifndef SDTW_START_PM
-#define SDTW_START_PM 1
+#define SDTW_START_PM 0
 #endif
 
 // lexicographic (cost, col): "a better than b"
@@ -743,9 +751,10 @@ __device__ __forceinline__ int fmod_pos(int a, int m) { int r = a % m; return r 
 __device__ __forceinline__ bool hits_row(int blo, int len, int row, int Pd) { return fmod_pos(row - blo, Pd) < len; }
 
 // ============================================================================ kernel
-template <int C, int WC, bool FMA, bool TRACE, bool CLUSTER, bool XS = false>
+template <int C, int WC, bool FMA, bool TRACE, bool CLUSTER, bool XS = false, bool CKPT = false>
 __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2) sdtw_dp_kernel(const DpParams P) {
     static_assert(!XS || C == 2, "single-row layout is for two chains");
+    static_assert(!CKPT || (!TRACE && !CLUSTER && SDTW_FAST_RUNS), "round checkpoints: cost/end kernels without clusters");
     static_assert(C == 1 || C == 2 || C == 4, "chains per lane");
     static_assert(((WC + 1) & WC) == 0 && (32 * C) % (WC + 1) == 0 && (WC + 1) % C == 0,
                   "rotation period U = WC+1 must be a power of two dividing 32*C and divisible by C");
@@ -859,6 +868,15 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     }
     const int Pl = pb - pa;                                 // rounds in this unit
     const int Mtot_bands = Pl * Pd;
+    // round checkpoints of this unit: local round l -> ckb + l*Pd (rows [0, Pd))
+    float* ckb = nullptr;
+    if constexpr (CKPT) {
+        const int kind = seg;
+        if (SPEC && P.utab && kind >= 2 * P.ck_sg)          // correction unit C_s, s = kind - 2Sg + 1
+            ckb = P.ckpt_c + ((long)q * (P.ck_sg - 1) + (kind - 2 * P.ck_sg)) * P.ck_rc * (long)PdMax;
+        else
+            ckb = P.ckpt + ((long)q * P.Pr + pa) * (long)PdMax;
+    }
 
     // ---- prologue: query rows -> smem, boundary ring (+inf, or the previous
     // segment's last column), counters
@@ -1214,6 +1232,20 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
 
         // ---- publish progress
         __syncwarp();
+        if constexpr (CKPT) {
+            // round checkpoints: the last warp copies the wrap-ring rows it wrote in this chunk
+            // (its last chain's bands t - u_max for t in [t0, t0+K); K < Pd, so none has been
+            // overwritten yet) to global memory -- coalesced, once per chunk, off the fast path
+            if (!has_succ_ring) {
+                for (int t = t0 + lane; t < t0 + K; t += 32) {
+                    const int b = t - u_max;
+                    if (b >= 0 && b < Mtot_bands) {
+                        const int pr = b / Pd, row = b - pr * Pd;
+                        ckb[(long)pr * PdMax + row] = bnd[row].d;
+                    }
+                }
+            }
+        }
         if (lane == 31) st_release_hop(succ_pp, t0 + K, succ_remote);
         if (lane == 0 && gw > 0) st_release_hop(pred_cp, t0 + K, pred_remote);
     }

@@ -155,9 +155,14 @@ def test_spec_constant_signals_ties():
     Q = np.zeros((3, 200), np.float32)
     c, e, fixed, _ = _run(Q, Y, OPT_SCHED=3)
     assert np.all(c == 0) and np.all(e == 0) and fixed == 0
-    # start index: the tie between boundary and free paths is not a strict win -> recompute
-    c, e, fixed, _, s = _run(Q, Y, start=True, OPT_SCHED=3)
+    # start index by forward propagation: the tie between boundary and free paths is not a
+    # strict win -> recompute
+    c, e, fixed, _, s = _run(Q, Y, start=True, OPT_SCHED=3, OPT_START=1)
     assert np.all(c == 0) and np.all(e == 0) and np.all(s == 0) and fixed == 3
+    # checkpointed start index: the cost/end DP's values are exact under ties
+    # (min of the two DPs), and the start comes from the walk-back on them -- no recompute
+    c, e, fixed, _, s = _run(Q, Y, start=True, OPT_SCHED=3, OPT_START=2)
+    assert np.all(c == 0) and np.all(e == 0) and np.all(s == 0) and fixed == 0
 
 
 def test_spec_errors():
