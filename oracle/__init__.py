@@ -45,6 +45,9 @@ def lib():
         L.oracle_walkback.restype = i64
         L.oracle_walkback_path.argtypes = [f32p, i64, i64, i64, i64p, i64p]
         L.oracle_walkback_path.restype = ctypes.c_int
+        u8p = ctypes.POINTER(ctypes.c_uint8)
+        L.oracle_sdtw_q8.argtypes = [u8p, i64, i64, u8p, i64, ctypes.c_int, i64p, i64p]
+        L.oracle_sdtw_q8.restype = ctypes.c_int
         L.oracle_round_half.argtypes = [ctypes.c_double, ctypes.c_double]
         L.oracle_round_half.restype = ctypes.c_float
         _lib = L
@@ -173,3 +176,65 @@ def sdtw_normalized(Q, Y, fma: bool = True, start: bool = False, threads: int | 
     Yn = znorm(np.asarray(Y, np.float32)[None, :])[0]
     Qn = znorm(Q)
     return sdtw(Qn, Yn, fma=fma, start=start, threads=threads)
+
+
+# ----------------------------------------------------------------------------------------
+# uint8 codebook (§Discussion)
+Q8_INF = 1 << 30
+
+
+def codebook(Y, clip_ppm: int = 1000):
+    """The reference codebook: "get the distribution of floating point values and
+    then evenly divide the bulk of the distribution across uint8 values clamping any
+    outliers to the extreme values".  Reading G18: the bulk is [lo, hi] with lo / hi the
+    order statistics (0-based ranks in the sorted samples) k and M-1-k,
+    k = floor(clip_ppm * (M-1) / 10^6) (integer arithmetic).  Returns (lo, hi) as fp32."""
+    y = np.sort(np.asarray(Y, np.float32).ravel(), kind="stable")
+    M = y.shape[0]
+    k = (int(clip_ppm) * (M - 1)) // 1_000_000
+    return np.float32(y[k]), np.float32(y[M - 1 - k])
+
+
+def quantize(v, lo, hi):
+    """uint8 codes (reading G19): "evenly divide" = 256 equal-width levels over [lo, hi],
+    code = clamp(floor((v - lo) * (255 / (hi - lo)) + 0.5), 0, 255) with every operation
+    one IEEE fp64 rounding (numpy evaluates the expression one operation at a time, no
+    contraction); hi == lo -> all codes 0."""
+    v = np.asarray(v, np.float32)
+    lo64, hi64 = np.float64(np.float32(lo)), np.float64(np.float32(hi))
+    if not hi64 > lo64:
+        return np.zeros(v.shape, np.uint8)
+    s = np.float64(255.0) / (hi64 - lo64)
+    u = (v.astype(np.float64) - lo64) * s + np.float64(0.5)
+    return np.clip(np.floor(u), 0.0, 255.0).astype(np.uint8)
+
+
+def sdtw_q8(Qc, Yc, tau: int = -1):
+    """Batched sDTW over uint8 codes (oracle_sdtw_q8 in sdtw_oracle.c): exact integer costs
+    (int64; Q8_INF = every path pruned) and the smallest argmin end.  tau < 0: no pruning."""
+    Qc = np.ascontiguousarray(Qc, dtype=np.uint8)
+    if Qc.ndim == 1:
+        Qc = Qc[None, :]
+    Yc = np.ascontiguousarray(Yc, dtype=np.uint8)
+    Z, N = Qc.shape
+    M = Yc.shape[0]
+    cost = np.empty(Z, np.int64)
+    end = np.empty(Z, np.int64)
+    u8p = ctypes.POINTER(ctypes.c_uint8)
+    rc = lib().oracle_sdtw_q8(Qc.ctypes.data_as(u8p), Z, N, Yc.ctypes.data_as(u8p), M, int(tau), _i64(cost), _i64(end))
+    if rc != 0:
+        raise ValueError("oracle_sdtw_q8: bad arguments")
+    return dict(cost=cost, end=end)
+
+
+def sdtw_q8_normalized(Q, Y, tau: int = -1, clip_ppm: int = 1000, normalize: bool = True):
+    """End-to-end uint8 oracle: z-normalise (as sdtw_normalized), codebook of the reference,
+    code both sides, integer DP.  Returns dict(cost, end, lo, hi, Qc, Yc)."""
+    Yn = znorm(np.asarray(Y, np.float32)[None, :])[0] if normalize else np.asarray(Y, np.float32)
+    Qn = znorm(Q) if normalize else np.asarray(Q, np.float32)
+    lo, hi = codebook(Yn, clip_ppm)
+    Yc = quantize(Yn, lo, hi)
+    Qc = quantize(Qn, lo, hi)
+    r = sdtw_q8(Qc, Yc, tau)
+    r.update(lo=lo, hi=hi, Qc=Qc, Yc=Yc)
+    return r

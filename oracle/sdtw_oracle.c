@@ -31,6 +31,8 @@
  *  Packed half (fma_mode == 2): the same recurrence with every value
  *  rounded to binary16 after each operation (oracle_round_half / oracle_cell16 below).
  *
+ *  uint8 codebook: oracle_sdtw_q8 below (exact integers).
+ *
  *  The normaliser (§5.1 Eq. 2) lives in oracle/__init__.py (znorm): its
  *  sums are exact (math.fsum), which plain C fp64 accumulation is not (reading G8).
  *
@@ -265,5 +267,61 @@ int oracle_walkback_path(const float* D, int64_t N, int64_t M, int64_t end, int6
     return 0;
 }
 
-/* z-normalisation of n_series contiguous series of length len (Eq. 2). */
-int oracle_abi_version(void) { return 1; }
+/* ---------------------------------------------------- uint8 codebook (NEXT-3)
+ * The paper's future-work variant (§Discussion): queries and reference as
+ * uint8 codes of one reference-derived codebook (the codes are made in oracle/__init__.py:
+ * codebook / quantize), the cell in exact integers, and "early pruning of values that have
+ * a large separation in distance": after the subtraction, a cell whose codes are more than
+ * tau apart returns INF "instead of performing multiplication".  Readings:
+ *     t = cx_i - cy_j;   D(i,j) = INF                               if tau >= 0 and |t| > tau
+ *                               = min(t*t + min(diag, up, left), INF)  otherwise
+ * INF = 2^30, the same virtual row (0) / column (INF) as the fp32 recurrence; cost = the
+ * last-row minimum (a cost of INF: every path crosses a pruned cell), end = the smallest
+ * column attaining it.  int64 throughout: nothing can overflow. */
+#define ORACLE_Q8_INF ((int64_t)1 << 30)
+
+static void oracle_q8_one(const uint8_t* X, int64_t N, const uint8_t* Y, int64_t M, int tau,
+                          int64_t* out_cost, int64_t* out_end, int64_t* prev, int64_t* cur)
+{
+    for (int64_t i = 0; i < N; ++i) prev[i] = ORACLE_Q8_INF;     /* column -1 */
+    int64_t best = ORACLE_Q8_INF + 1, best_j = 0;
+    for (int64_t j = 0; j < M; ++j) {
+        for (int64_t i = 0; i < N; ++i) {
+            int64_t up = (i == 0) ? 0 : cur[i - 1];
+            int64_t diag = (i == 0) ? 0 : prev[i - 1];
+            int64_t left = prev[i];
+            int64_t m = diag;
+            if (up < m) m = up;
+            if (left < m) m = left;
+            int64_t t = (int64_t)X[i] - (int64_t)Y[j];
+            int64_t v;
+            if (tau >= 0 && (t > tau || -t > tau)) {
+                v = ORACLE_Q8_INF;
+            } else {
+                v = t * t + m;
+                if (v > ORACLE_Q8_INF) v = ORACLE_Q8_INF;
+            }
+            cur[i] = v;
+        }
+        if (cur[N - 1] < best) { best = cur[N - 1]; best_j = j; }
+        int64_t* tp = prev; prev = cur; cur = tp;
+    }
+    *out_cost = best;
+    *out_end = best_j;
+}
+
+/* Batched uint8 sDTW: Q row-major Z x N codes, Y[M] codes, tau < 0 (or >= 255): no pruning.
+ * Returns 0, or 1 on bad arguments. */
+int oracle_sdtw_q8(const uint8_t* Q, int64_t Z, int64_t N, const uint8_t* Y, int64_t M, int tau,
+                   int64_t* cost, int64_t* end)
+{
+    if (Z < 0 || N < 1 || M < 1 || (Z > 0 && (!Q || !Y || !cost || !end))) return 1;
+    int64_t* prev = (int64_t*)malloc(sizeof(int64_t) * N);
+    int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * N);
+    for (int64_t q = 0; q < Z; ++q) oracle_q8_one(Q + q * N, N, Y, M, tau, &cost[q], &end[q], prev, cur);
+    free(prev);
+    free(cur);
+    return 0;
+}
+
+int oracle_abi_version(void) { return 2; }
