@@ -39,7 +39,7 @@ sys.path.insert(0, ROOT)
 
 # ALU roofline: SMs x 128 FP32 lanes x f_SM / (SASS issue slots per cell)
 LANES_PER_SM = 128
-SASS_PER_CELL = {"half2": 1.5, "packed_fma": 2.0, "scalar_fma": 3.0, "scalar_nofma": 4.0, "packed_nofma": 3.5,
+SASS_PER_CELL = {"q8": 3.0, "q8_prune": 6.0, "half2": 1.5, "packed_fma": 2.0, "scalar_fma": 3.0, "scalar_nofma": 4.0, "packed_nofma": 3.5,
                  "packed_fma_trace": 6.0, "scalar_fma_trace": 7.0}
 
 
@@ -164,6 +164,19 @@ def _workload(cfg_name: str, rank: int, world: int, scaling: str):
         return Q, Y, dict(Z=Zg, Z_local=Zl, N=N, M=M, seed=seed, start=cfg["start"], offsets=off,
                           cells_local=float(off[-1]) * M)
     Q = nanopore_queries(Zl, N, M, seed, first_query=first)
+    if cfg.get("straddle"):
+        # every `every`-th query: a copy of the reference compressed `stride`x, placed 500..2,800
+        # columns before a boundary of the 6-segment speculative plan (OPT_SEGMENTS=6 is set
+        # for this config; boundaries = floor(s*Pr/6) rounds x columns per round), so its match
+        # crosses the boundary for longer than the correction pass (2 rounds = 7,680 columns)
+        import paper_2403_06931_b200 as sd
+        from datagen import straddle_queries
+        every, stride = cfg["straddle"]
+        cols = sd.round_columns(N)
+        Pr = -(-M // cols)
+        ks = [k for k in range(Zl) if (first + k) % every == 0]
+        pos = [(((1 + j % 5) * Pr) // 6) * cols - 500 - 37 * (j // 5) for j in range(len(ks))]
+        Q[ks] = straddle_queries(Y, pos, N, stride, seed)
     return Q, Y, dict(Z=Zg, Z_local=Zl, N=N, M=M, seed=seed, start=cfg["start"])
 
 
@@ -263,6 +276,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--half", action="store_true",
                     help="packed-half precision (SDTW_OPT_PRECISION=16, SURVEY NEXT-1: the paper's __half2)")
+    ap.add_argument("--q8", action="store_true",
+                    help="uint8 codebook (sdtw_batch_q8, SURVEY NEXT-3, PAPER.md P:L165): integer cells")
+    ap.add_argument("--q8-prune", type=int, default=-1,
+                    help="with --q8: INF-prune cells whose codes differ by more than TAU (-1: off)")
     ap.add_argument("--path", action="store_true",
                     help="step = sdtw_path (start index + full warp path, SURVEY NEXT-2)")
     args = ap.parse_args()
@@ -294,7 +311,11 @@ def main():
     from paper_2403_06931_b200.distributed import distributed_batch
     if args.half:
         sd.set_option(sd.OPT_PRECISION, 16)
+    if args.q8:
+        sd.set_option(sd.OPT_Q8_PRUNE, args.q8_prune)
 
+    if args.config == "c3_straddle":
+        sd.set_option(sd.OPT_SEGMENTS, 6)
     Q, Y, w = _workload(args.config, rank, world, args.scaling)
     N, M = w["N"], w["M"]
     trace = bool(w["start"])
@@ -318,6 +339,8 @@ def main():
             return distributed_batch(Qd, traceback=trace, pre_sharded=True, device=dev, path=args.path)
         if args.path:
             return sd.path(Qd)
+        if args.q8:
+            return sd.batch_q8(Qd)
         return sd.traceback(Qd) if trace else sd.batch(Qd)
 
     for _ in range(args.warmup):
@@ -364,6 +387,8 @@ def main():
     packed = popt > 0 or (popt < 0 and (not trace or ckpt_start))
     mix = "half2" if args.half else ("packed" if packed else "scalar") + "_fma" + (
         "_trace" if trace and not ckpt_start else "")
+    if args.q8:
+        mix = "q8_prune" if 0 <= args.q8_prune < 255 else "q8"
     k = SASS_PER_CELL[mix]
     peak = sms * LANES_PER_SM * fmax * 1e6 / k / 1e9
     peak3 = sms * LANES_PER_SM * fmax * 1e6 / 3.0 / 1e9
@@ -371,13 +396,13 @@ def main():
     achieved = (w["cells_local"] if ragged else float(w["Z_local"]) * N * M) / (dp_avg / 1e3) / 1e9
     clocks = sampler.summary()
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "GCUPS", "frac": achieved / peak,
-            "traffic": _traffic(args.config, w, 16 if args.half else 32), "sass_per_cell": k, "peak_source": "%s sm_max_mhz=%.0f x %d SMs x %d lanes / %g"
+            "traffic": _traffic(args.config, w, 16 if args.half else (8 if args.q8 else 32)), "sass_per_cell": k, "peak_source": "%s sm_max_mhz=%.0f x %d SMs x %d lanes / %g"
             % (src, fmax, sms, LANES_PER_SM, k),
             "headline_peak_k3": peak3, "headline_frac_k3": achieved / peak3,
             "dp_kernel_ms": dp_avg}
     if clocks.get("sm_mhz"):
         roof["frac_at_sampled_clock"] = achieved / (peak * clocks["sm_mhz"] / fmax)
-    meas = _issue_counts(args.config, w, 16 if args.half else 32)
+    meas = _issue_counts(args.config, w, 16 if args.half else (8 if args.q8 else 32))
     if meas:
         roof.update(meas)
     if ckpt_start:
@@ -395,7 +420,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         Qh = torch.from_numpy(Q).pin_memory()
-        api = sd.path if args.path else (sd.traceback if trace else sd.batch)
+        api = sd.path if args.path else (sd.traceback if trace else (sd.batch_q8 if args.q8 else sd.batch))
         if ragged:
             api = lambda q: sd.batch_ragged(q, w["offsets"])  # noqa: E731
         api(Qh.numpy())
@@ -432,7 +457,8 @@ def main():
         line = {
             "metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": "f16" if args.half else "f32",
+            "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "f16" if args.half else ("i32 (u8 codes)" if args.q8 else "f32"),
             "data": "synthetic nanopore-like signals (datagen, seeded); random reference, no trained weights",
             "config": {"workload": "%s: %d x %d queries vs %d-sample reference%s" % (
                 args.config, w["Z"], N, M, " (start index on)" if trace else ""),
@@ -448,6 +474,18 @@ def main():
             "gsps_eq3": gsps(float(w["Z"]) * N, tot_ms / args.steps),
             "e2e": e2e, "cpu_baseline": cpu,
         }
+        if args.q8:
+            # accuracy metric of the approximation: end index of the uint8 path
+            # against the fp32 path (bit-exact with the fp32 oracle) on this batch, untimed
+            cq, eq = step()
+            ef = sd.batch(Qd)[1]
+            d = (eq.to(torch.int64) - ef).abs()
+            line["q8"] = {"prune_tau": args.q8_prune, "codebook": [float(v) for v in sd.q8_codebook()],
+                          "end_exact_vs_fp32": float((d == 0).double().mean().item()),
+                          "end_within_8_vs_fp32": float((d <= 8).double().mean().item()),
+                          "all_paths_pruned": int((cq >= (1 << 30)).sum().item())}
+            line["config"]["workload"] += " (uint8 codebook%s)" % (
+                ", INF pruning tau=%d" % args.q8_prune if 0 <= args.q8_prune < 255 else "")
         if args.path:
             import torch as _t
             c, e, st, lo, hi = [_t.as_tensor(np.asarray(a.cpu() if hasattr(a, "cpu") else a)) for a in step()]

@@ -84,12 +84,26 @@ enum {
                                the segment's own); 0 = auto (>= 3 query lengths).  A segment
                                whose correction is not overtaken in time is recomputed, so
                                any value gives exact results; it only moves work */
-    SDTW_OPT_PRECISION = 14 /* 32 (default): fp32 cells, bit-exact with the fp32 oracle;
+    SDTW_OPT_PRECISION = 14,/* 32 (default): fp32 cells, bit-exact with the fp32 oracle;
                                16: packed half (the paper's __half2):
                                queries/reference rounded to binary16, every cell op rounded to
                                binary16 (HADD2, HFMA2, 3-input half2 min); costs overflow to
-                               +inf above 65504; sdtw_batch / sdtw_batch_ragged only
+                               +inf above 65504;
+                               8: uint8 codebook (the paper's future work P:L165;
+                               DESIGN.md §16): reference and queries coded 0..255 through the
+                               reference's codebook (sdtw_q8_codebook), integer cell
+                               (cx - cy)^2 + min(...), optional INF pruning (SDTW_OPT_Q8_PRUNE);
+                               sdtw_batch returns cost x delta^2 (delta = (hi - lo)/255) in fp32,
+                               sdtw_batch_q8 the exact integer cost; N <= 12,000.
+                               16 and 8: sdtw_batch / sdtw_batch_ragged / sdtw_batch_q8 only
                                (no start index), no clusters, OPT_PACKED ignored, W in {30, 62} */
+    SDTW_OPT_Q8_PRUNE = 18, /* uint8 codebook: INF pruning of "far" cells: a cell with
+                               |cx - cy| > tau is INF (2^30: no path through it); -1 (default)
+                               or tau >= 255: off */
+    SDTW_OPT_Q8_CLIP = 19   /* uint8 codebook: tail mass clamped to each extreme code, in parts
+                               per million of the reference (default 1000 = 0.1 %); the
+                               codebook spans the order statistics of rank k and M-1-k,
+                               k = floor(clip * (M-1) / 1e6) */
 };
 
 /* Install the reference Y[M] on the current device (copied into a
@@ -189,6 +203,26 @@ sdtw_status sdtw_boundary_dp(const float* Q, int64_t n_queries, int64_t N, const
 sdtw_status sdtw_columns_dominate(const float* B, const float* F, int64_t n_queries, int64_t N, int32_t* out_flag);
 sdtw_status sdtw_merge_candidates(const float* cost, const int64_t* end, const int32_t* valid, int64_t n_sets,
                                   int64_t n_queries, float* out_cost, int64_t* out_end, int32_t* out_invalid);
+
+/* uint8-codebook sDTW (§Discussion).
+ *
+ * sdtw_q8_codebook: *lo, *hi = the codebook of the current reference (its order statistics of
+ * rank k and M-1-k, k = floor(SDTW_OPT_Q8_CLIP * (M-1) / 1e6), of the reference as installed,
+ * i.e. normalised when SDTW_OPT_NORMALIZE=1); built on first use after sdtw_set_reference.
+ *
+ * sdtw_quantize: out[i] = clamp(floor((in[i] - lo) * (255 / (hi - lo)) + 0.5), 0, 255), every
+ * operation one fp64 rounding (hi == lo: 0).  in: n fp32, out: n bytes; host or device.
+ *
+ * sdtw_batch_q8: sdtw_batch with SDTW_OPT_PRECISION=8 whatever the option says, returning the
+ * exact integer cost: out_cost[q] = min_j D(N-1, j) over the integer recurrence
+ *     D(i,j) = INF                                    if |cx_i - cy_j| > tau (pruning on)
+ *            = min((cx_i - cy_j)^2 + min(D(i-1,j), D(i,j-1), D(i-1,j-1)), INF)   otherwise,
+ * INF = 2^30 (a cost of INF: every path crosses a pruned cell); out_end[q] = smallest argmin.
+ * Queries are z-normalised first when SDTW_OPT_NORMALIZE=1, then coded.  N <= 12,000.
+ * Pointers host or device.  Errors: as sdtw_batch, SDTW_E_ARG for N > 12,000. */
+sdtw_status sdtw_q8_codebook(float* lo, float* hi);
+sdtw_status sdtw_quantize(const float* in, int64_t n, uint8_t* out);
+sdtw_status sdtw_batch_q8(const float* Q, int64_t n_queries, int64_t N, int32_t* out_cost, int64_t* out_end);
 
 /* z-normalisation of n_series contiguous series of length len (the paper's
  * runNormalizer; Eq. 2 P:L73 with the population variance of P:L85-L86):

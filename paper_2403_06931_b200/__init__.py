@@ -7,7 +7,8 @@ fallback: importing this package fails loudly when the library is missing, and
 every call raises when the CUDA path fails.
 
 Functions mirror the ABI names (minus the ``sdtw_`` prefix):
-``set_reference``, ``batch``, ``batch_ragged``, ``traceback``, ``path``, ``znormalize``, ``set_option``,
+``set_reference``, ``batch``, ``batch_ragged``, ``traceback``, ``path``, ``znormalize``, ``batch_q8``,
+``q8_codebook``, ``quantize``, ``set_option``,
 ``get_option``, ``profile``, ``launch_count``, ``release``.
 Inputs may be torch tensors (CUDA or CPU) or numpy arrays.  torch supplies
 device memory and the current stream (passed as SDTW_OPT_STREAM).
@@ -53,20 +54,24 @@ _lib.sdtw_boundary_dp.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, 
 _lib.sdtw_columns_dominate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _i64, _i64, ctypes.c_void_p]
 _lib.sdtw_merge_candidates.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, _i64, _i64, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p]
+_lib.sdtw_batch_q8.argtypes = [ctypes.c_void_p, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p]
+_lib.sdtw_q8_codebook.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
+_lib.sdtw_quantize.argtypes = [ctypes.c_void_p, _i64, ctypes.c_void_p]
 _lib.sdtw_launch_count.restype = _i64
 _lib.sdtw_last_error.restype = ctypes.c_char_p
 _lib.sdtw_version.restype = ctypes.c_int
 _lib.sdtw_build_info.restype = ctypes.c_char_p
 for _n in ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sdtw_traceback", "sdtw_path", "sdtw_znormalize",
            "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_spec_recomputed", "sdtw_round_columns",
-           "sdtw_batch_columns", "sdtw_boundary_dp", "sdtw_columns_dominate", "sdtw_merge_candidates"):
+           "sdtw_batch_columns", "sdtw_boundary_dp", "sdtw_columns_dominate", "sdtw_merge_candidates",
+           "sdtw_batch_q8", "sdtw_q8_codebook", "sdtw_quantize"):
     getattr(_lib, _n).restype = ctypes.c_int
 
 # ABI constants (include/sdtw.h)
 OK, E_ARG, E_NOREF, E_CUDA, E_NOMEM, E_NONFINITE = range(6)
 OPT_NORMALIZE, OPT_FMA, OPT_SEGMENT_W, OPT_LANES, OPT_CLUSTER, OPT_STREAM, OPT_PACKED, OPT_CHUNK, \
     OPT_PROFILE, OPT_RING, OPT_SCHED, OPT_SEGMENTS, OPT_WORKERS, OPT_PRECISION, OPT_PAD, \
-    OPT_SPEC_ROUNDS, OPT_START = range(1, 18)
+    OPT_SPEC_ROUNDS, OPT_START, OPT_Q8_PRUNE, OPT_Q8_CLIP = range(1, 20)
 _STATUS = {0: "SDTW_OK", 1: "SDTW_E_ARG", 2: "SDTW_E_NOREF", 3: "SDTW_E_CUDA", 4: "SDTW_E_NOMEM",
            5: "SDTW_E_NONFINITE"}
 
@@ -74,6 +79,7 @@ EXPORTED_SYMBOLS = ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sd
                     "sdtw_set_option", "sdtw_get_option", "sdtw_profile", "sdtw_spec_recomputed", "sdtw_launch_count",
                     "sdtw_round_columns", "sdtw_batch_columns", "sdtw_boundary_dp",
                     "sdtw_columns_dominate", "sdtw_merge_candidates",
+                    "sdtw_batch_q8", "sdtw_q8_codebook", "sdtw_quantize",
                     "sdtw_last_error", "sdtw_release", "sdtw_version", "sdtw_build_info")
 
 
@@ -172,6 +178,44 @@ def batch(Q):
     _bind_stream(keep)
     _check(_lib.sdtw_batch(ctypes.c_void_p(ptr), Z, N, ctypes.c_void_p(pc), ctypes.c_void_p(pe)))
     return cost, end
+
+
+def batch_q8(Q):
+    """sdtw_batch_q8 (uint8 codebook): Q [Z, N] -> (cost[Z] int32, the exact
+    integer cost; end[Z] int64) on Q's device (numpy if host).  Pruning: OPT_Q8_PRUNE."""
+    keep, ptr, shape = _as_f32(Q)
+    if len(shape) == 1:
+        shape = (1, shape[0])
+    Z, N = shape
+    cost, end, _, (pc, pe, _) = _outputs(keep, Z, False)
+    torch = _torch()
+    cost = cost.view(torch.int32) if torch is not None and isinstance(cost, torch.Tensor) else cost.view(np.int32)
+    _bind_stream(keep)
+    _check(_lib.sdtw_batch_q8(ctypes.c_void_p(ptr), Z, N, ctypes.c_void_p(pc), ctypes.c_void_p(pe)))
+    return cost, end
+
+
+def q8_codebook():
+    """sdtw_q8_codebook: (lo, hi) of the current reference's uint8 codebook."""
+    lo, hi = ctypes.c_float(), ctypes.c_float()
+    _check(_lib.sdtw_q8_codebook(ctypes.byref(lo), ctypes.byref(hi)))
+    return np.float32(lo.value), np.float32(hi.value)
+
+
+def quantize(X):
+    """sdtw_quantize: uint8 codes of X under the current codebook (same device as X)."""
+    keep, ptr, shape = _as_f32(X)
+    n = int(np.prod(shape)) if len(shape) else 1
+    torch = _torch()
+    if torch is not None and isinstance(keep, torch.Tensor) and keep.is_cuda:
+        out = torch.empty(shape, dtype=torch.uint8, device=keep.device)
+        po = out.data_ptr()
+    else:
+        out = np.empty(shape, np.uint8)
+        po = out.ctypes.data
+    _bind_stream(keep)
+    _check(_lib.sdtw_quantize(ctypes.c_void_p(ptr), n, ctypes.c_void_p(po)))
+    return out
 
 
 def round_columns(N: int) -> int:

@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsdtw.so")
 SOURCES = (["sdtw_api.cu"] + ["sdtw_dp_c%d%s.cu" % (c, t) for c in (1, 2, 4) for t in ("", "t")]
-           + ["sdtw_dpq_c1.cu", "sdtw_dpq_c2.cu", "sdtw_dp16.cu", "sdtw_dp_c2k.cu"])
-HEADERS = ["sdtw_dp.cuh", "sdtw_dpq.cuh", "sdtw_prep.cuh", "sdtw_path.cuh", "sdtw_dp16.cuh", "sdtw_dp_pick.h"]
+           + ["sdtw_dpq_c1.cu", "sdtw_dpq_c2.cu", "sdtw_dp16.cu", "sdtw_dp8.cu", "sdtw_dp_c2k.cu"])
+HEADERS = ["sdtw_dp.cuh", "sdtw_dpq.cuh", "sdtw_prep.cuh", "sdtw_path.cuh", "sdtw_dp2.cuh", "sdtw_q8.cuh", "sdtw_start.cuh", "sdtw_dp_pick.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

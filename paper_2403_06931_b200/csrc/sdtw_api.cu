@@ -8,7 +8,7 @@
 #include "sdtw_dp.cuh"
 #include "sdtw_dp_pick.h"
 #include "sdtw_dpq.cuh"
-#include "sdtw_dp16.cuh"
+#include "sdtw_q8.cuh"
 #include "sdtw_path.cuh"
 #include "sdtw_prep.cuh"
 #include "sdtw_start.cuh"
@@ -39,7 +39,11 @@ struct Options {
     int sched = 0;       // 0 auto, 1 one CTA (or cluster) per query, 2 persistent segments
     int segments = 0;
     int workers = 0;     // resident CTAs per SM under persistent scheduling (0 = auto)
-    int precision = 32;  // 32 fp32 cells; 16 packed half (sdtw_dp16.cuh)
+    int precision = 32;  // 32 fp32 cells; 16 packed half; 8 uint8 codebook (sdtw_dp2.cuh, sdtw_q8.cuh)
+    int q8_prune = -1;   // uint8 codebook: INF-pruning threshold tau in code units (-1 = off)
+    int q8_clip = 1000;  // uint8 codebook: clipped tail mass per side, parts per million
+    int q8_codes_in = 0; // (internal) the batch already holds codes (speculative recomputation)
+    int q8_int_out = 0;  // (internal) sdtw_batch_q8: leave the integer costs
     int pad = 0;         // extra idle rows per round period (0 = auto)
     int spec_rounds = 0; // speculative segments: rounds per correction pass (0 = auto)
     int start = 0;       // start index: 0 auto, 1 forward propagation, 2 checkpoints + walk-back
@@ -74,6 +78,13 @@ struct Ctx {
     int last_start_iters = 0;                       // ... and its window-widening iterations
     int64_t last_fixups = 0;                        // queries recomputed by the last call
     int64_t order_key[3] = {-1, -1, -1};
+    // uint8 codebook (NEXT-3, sdtw_q8.cuh): codes of the reference as fp32 0..255 (Malloc,
+    // padded 0), the codebook {lo, hi} on the device and host, radix-select workspace
+    float* ref_q8 = nullptr;
+    unsigned char* q8_ws = nullptr;                 // 2 x 65536 counters + selections + codebook
+    int q8_clip = -1;                               // clip of the current codes (-1: none built)
+    float q8_lo = 0.f, q8_hi = 0.f;
+    float* ws_xq = nullptr;  size_t ws_xq_n = 0;    // query codes
     int* flag_d = nullptr;
     int* flag_h = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -149,9 +160,13 @@ using sdtw::DpParams;
 using sdtw::DpKernel;
 
 // dual: the dual-query kernel (two queries per lane, C chains of scalar-y strips)
-DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl, bool dual = false, bool half = false,
+// half: 0 fp32; 16 packed half; 8 / 9 uint8 codebook without / with INF pruning
+DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl, bool dual = false, int half = 0,
                      bool xs = false) {
-    if (half) return (C == 2 && !trace && !cl && !dual) ? sdtw::pick_dp16(WC) : nullptr;
+    if (half) {
+        if (C != 2 || trace || cl || dual) return nullptr;
+        return half == 16 ? sdtw::pick_dp16(WC) : sdtw::pick_dp8(WC, half == 9);
+    }
     if (xs) return (C == 2 && !trace && !cl && !dual) ? sdtw::pick_dp_c2xs(WC, fma) : nullptr;
     if (dual) {
         if (cl) return nullptr;
@@ -166,7 +181,7 @@ struct LaunchCfg {
     int dual;        // two queries per lane (chains per lane = C)
     int64_t units;   // rings per batch: queries, or query pairs when dual
     int need;        // V + (G+1)K: smallest ring-safe round period (ragged batches: per query)
-    int half;        // packed-half kernel (SDTW_OPT_PRECISION = 16)
+    int half;        // two-chain reduced-precision kernel: 16 packed half, 8 / 9 uint8 codebook (9: INF pruning)
     int xs;          // single-row query layout (long queries)
     int spec = 0;    // speculative segments: Sseg segments, correction passes of Rc rounds
     int Sseg = 0, Rc = 0;
@@ -179,6 +194,11 @@ struct Ragged {
     int64_t nmin = 0;
 };
 
+int smem2_bytes(int half, int WC, int GW, int Pd, int RS) {
+    return half == 16 ? sdtw::smem_layout2<sdtw::Half2Arith>(WC, GW, Pd, RS).bytes
+                      : sdtw::smem_layout2<sdtw::Q8Arith<false>>(WC, GW, Pd, RS).bytes;
+}
+
 // Schedule choice.  OPT_PACKED: 0 scalar (C=1), 1 two packed chains (C=2), 2 four
 // chains (C=4), 3 dual-query x 2 chains, 4 dual-query x 1 chain; -1 auto.
 sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cfg, const Ragged* rg = nullptr) {
@@ -186,9 +206,10 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // auto: two packed chains (f32x2) for cost/end; scalar strips for the start-index
     // variant, whose per-cell start selects double the registers per slot (r01 sweep at
     // N=1000: scalar W=15 3.00, packed W=14 2.89, packed W=30 1.80 TCUPS)
-    const bool half = o.precision == 16;
-    if (half && trace) return fail(SDTW_E_ARG, "the packed-half precision has no start index (OPT_PRECISION=32)");
-    if (half && o.cluster > 1) return fail(SDTW_E_ARG, "the packed-half precision runs without clusters");
+    const int half = o.precision == 16 ? 16 : (o.precision == 8 ? (o.q8_prune >= 0 && o.q8_prune < 255 ? 9 : 8) : 0);
+    if (half && trace) return fail(SDTW_E_ARG, "the packed-half and uint8 precisions have no start index (OPT_PRECISION=32)");
+    if (half && o.cluster > 1) return fail(SDTW_E_ARG, "the packed-half and uint8 precisions run without clusters");
+    if (half && half != 16 && N > sdtw::kQ8MaxN) return fail(SDTW_E_ARG, "the uint8 precision takes queries of <= 12,000 samples");
     const int packed = half ? 1 : (o.packed < 0 ? (trace ? 0 : 1) : o.packed);
     const bool dual = packed >= 3;
     int C = dual ? (packed == 3 ? 2 : 1) : (packed == 0 ? 1 : (packed == 1 ? 2 : 4));
@@ -230,7 +251,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
             const int pd = (int)(N > nd ? N : nd);
             int rs = 1;
             while (rs < std::max(4 * k, 64)) rs <<= 1;
-            return half ? sdtw::smem_layout16(WC, GW, pd, rs).bytes : sdtw::smem_layout(C, WC, trace, GW, pd, rs).bytes;
+            return half ? smem2_bytes(half, WC, GW, pd, rs) : sdtw::smem_layout(C, WC, trace, GW, pd, rs).bytes;
         };
         auto ctas = [&](int bytes) { return (int)((228 * 1024) / (bytes + 1024)); };
         const int base = ctas(bytes_for(K));
@@ -249,9 +270,8 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     while (RS < RSmin) RS <<= 1;
     auto layout = [&](int rs) {
         if (half) {
-            const sdtw::SmemLayout16 l = sdtw::smem_layout16(WC, GW, (int)Pd, rs);
             sdtw::SmemLayout r;
-            r.bytes = l.bytes;
+            r.bytes = smem2_bytes(half, WC, GW, (int)Pd, rs);
             return r;
         }
         return dual ? sdtw::smem_layout_q(C, WC, trace, GW, (int)Pd, rs) : sdtw::smem_layout(C, WC, trace, GW, (int)Pd, rs);
@@ -276,7 +296,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
         if (ctas(L.bytes) < 3 && ctas(Lx.bytes) > ctas(L.bytes)) { L = Lx; xs = true; }
     }
     *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0, dual ? 1 : 0, units, (int)need,
-                     half ? 1 : 0, xs ? 1 : 0};
+                     half, xs ? 1 : 0};
     // Persistent scheduling (default when a cluster is not requested): k resident CTAs
     // per SM, k = min(occupancy, rings / SMs), pull (ring, round-segment) units, so every
     // SM carries the same load whatever the batch size mod #SMs is.
@@ -351,7 +371,7 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
 
 sdtw_status launch_dp(const LaunchCfg& c, bool fma, bool trace, const DpParams& p, cudaStream_t st) {
     DpKernel k = c.ck ? sdtw::pick_dp_c2ck(c.WC, fma, c.xs != 0)
-                      : pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0, c.half != 0, c.xs != 0);
+                      : pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0, c.half, c.xs != 0);
     if (!k) return fail(SDTW_E_ARG, "no kernel for this configuration");
     CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem));
     if (c.CL > 8) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -465,6 +485,44 @@ struct SegReq {
     int ck_Pr = 0, ck_Pd = 0;      // mode 3: the layout the caller allocated (must match the plan)
 };
 
+// The uint8 codebook of the current reference: two exact order statistics
+// by radix select, then the reference codes.  Rebuilt when the reference or the clip
+// option changed.  Untimed setup (once per reference).
+constexpr size_t kQ8Hist = 2 * 65536 * sizeof(unsigned);
+sdtw_status ensure_q8(Ctx* ctx, cudaStream_t st) {
+    const int clip = g_opt.q8_clip;
+    if (ctx->ref_q8 && ctx->q8_clip == clip) return SDTW_OK;
+    if (!ctx->q8_ws) CK(cudaMalloc(&ctx->q8_ws, kQ8Hist + 256));
+    if (!ctx->ref_q8) CK(cudaMalloc(&ctx->ref_q8, ctx->Malloc * sizeof(float)));
+    unsigned* hist = reinterpret_cast<unsigned*>(ctx->q8_ws);
+    sdtw::Q8Sel* sel = reinterpret_cast<sdtw::Q8Sel*>(ctx->q8_ws + kQ8Hist);
+    float* cb = reinterpret_cast<float*>(ctx->q8_ws + kQ8Hist + 2 * sizeof(sdtw::Q8Sel));
+    const int64_t M = ctx->M;
+    const unsigned k_lo = (unsigned)(((int64_t)clip * (M - 1)) / 1000000);
+    const unsigned k_hi = (unsigned)(M - 1 - k_lo);
+    const int grid = 4 * ctx->sms;
+    for (int pass = 0; pass < 2; ++pass) {
+        CK(cudaMemsetAsync(hist, 0, kQ8Hist, st));
+        sdtw::q8_hist_kernel<<<grid, 256, 0, st>>>(ctx->ref, M, hist, sel, pass);
+        sdtw::q8_select_kernel<<<1, 1024, 0, st>>>(hist, sel, pass, k_lo, k_hi);
+        g_launches += 2;
+    }
+    sdtw::q8_codebook_kernel<<<1, 32, 0, st>>>(sel, cb);
+    sdtw::q8_quantize_kernel<<<grid, 256, 0, st>>>(ctx->ref, M, ctx->Malloc, cb, ctx->ref_q8);
+    g_launches += 2;
+    CK(cudaGetLastError());
+    float h[2];
+    CK(cudaMemcpyAsync(h, cb, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->q8_lo = h[0];
+    ctx->q8_hi = h[1];
+    ctx->q8_clip = clip;
+    return SDTW_OK;
+}
+const float* q8_codebook_dev(const Ctx* ctx) {
+    return reinterpret_cast<const float*>(ctx->q8_ws + kQ8Hist + 2 * sizeof(sdtw::Q8Sel));
+}
+
 sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int64_t* out_end,
                       int64_t* out_start, bool trace, BatchDev* dev_out = nullptr, Ragged rg = Ragged(),
                       const SegReq* sr = nullptr);
@@ -473,7 +531,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
 // (fix[q] != 0) are recomputed with sequential segments from their normalised rows and
 // their results replace the speculative ones.
 sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const std::vector<int64_t>* off,
-                       const int* fix_d, float* dc, int64_t* de, int64_t* ds, cudaStream_t st,
+                       const int* fix_d, float* dc, int64_t* de, int64_t* ds, cudaStream_t st, int Rc,
                        float* col_last = nullptr, const SegReq* ckr = nullptr) {
     std::vector<int> fix((size_t)Z);
     CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -514,6 +572,7 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
     const Options saved = g_opt;
     g_opt.normalize = 0;
     g_opt.profile = 0;
+    g_opt.q8_codes_in = 1;                            // uint8 codebook: rows are codes already
     g_opt.sched = 1;                                  // one CTA per ring: no speculation again
     g_opt.stream = st;
     const int64_t fixed_before = F;
@@ -539,6 +598,16 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
         r2.col_out = fcol;
         s = run_batch(rows, F, N, fc, fe, nullptr, false, nullptr, Ragged(), &r2);
     } else {
+        // The recomputed queries run through the speculative schedule again, with corrections
+        // four times as long (a match that straddled a segment boundary for more than Rc
+        // rounds); all SMs share the few queries instead of one CTA each (one CTA per query:
+        // ~1.4 s per 10M-sample query, a cliff on top of a 1.2 s batch).  Queries that fail
+        // again recurse with 16 Rc, ...; once the corrections no longer fit (Pr < 4(Rc+1))
+        // the plan falls back to sequential segments, so the recursion ends.
+        g_opt.sched = 0;
+        g_opt.spec_rounds = 4 * std::max(Rc, 1);
+        g_opt.segments = 0;
+        g_opt.workers = 0;
         s = run_batch(rows, F, off ? nmax2 : N, fc, fe, ds ? fs : nullptr, ds != nullptr, nullptr, rg2);
     }
     g_opt = saved;
@@ -716,6 +785,19 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     }
     CK(cudaGetLastError());
     g_launches++;
+    if (cfg.half == 8 || cfg.half == 9) {                // uint8 codebook: query codes
+        s = ensure_q8(ctx, st);
+        if (s != SDTW_OK) return s;
+        if (!o.q8_codes_in) {
+            s = grow(&ctx->ws_xq, &ctx->ws_xq_n, nel);
+            if (s != SDTW_OK) return s;
+            sdtw::q8_quantize_kernel<<<4 * ctx->sms, 256, 0, st>>>(xd, (int64_t)nel, (int64_t)nel, q8_codebook_dev(ctx),
+                                                                  ctx->ws_xq);
+            CK(cudaGetLastError());
+            g_launches++;
+            xd = ctx->ws_xq;
+        }
+    }
 
     // outputs: direct when device pointers, else staged
     const bool host_out = (kc == 0 || ke == 0 || ks == 0);
@@ -731,7 +813,8 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     }
     DpParams p;
     p.X = xd;
-    p.Y = ctx->ref;
+    p.Y = (cfg.half == 8 || cfg.half == 9) ? ctx->ref_q8 : ctx->ref;
+    p.q8_tau2 = cfg.half == 9 ? o.q8_prune * o.q8_prune : 0;
     p.Malloc = (int)ctx->Malloc;
     p.Z = (int)cfg.units;
     p.Zq = (int)Z;
@@ -776,7 +859,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     int* fix_d = nullptr;
     ctx->last_fixups = 0;
     if (cfg.persistent) {
-        const size_t ent = cfg.half ? 2 : (trace ? 8 : 4) * (cfg.dual ? 2 : 1);
+        const size_t ent = cfg.half == 16 ? 2 : (trace ? 8 : 4) * (cfg.dual ? 2 : 1);
         const size_t R = (size_t)cfg.units;
         // done flags: per ring (sequential segments: a counter) or per unit (speculative)
         const size_t done_b = ((sizeof(int) * R * (cfg.spec ? cfg.S : 1) + 255) / 256) * 256;
@@ -855,7 +938,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     } else if (cfg.spec) {
         sdtw::finalize_spec_kernel<<<(unsigned)Z, 128, 0, st>>>(
             static_cast<const sdtw::Partial*>(p.cand), p.bnd_g, (int)Z, cfg.S, cfg.Sseg,
-            cfg.Pd, (int)N, qlen_d, ctx->flag_d, dc, de, trace ? ds : nullptr, fix_d, cfg.half);
+            cfg.Pd, (int)N, qlen_d, ctx->flag_d, dc, de, trace ? ds : nullptr, fix_d, cfg.half == 16);
         CK(cudaGetLastError());
         g_launches++;
         if (smode == 1) {                                   // free-DP columns of kinds A_0 and B_{Sg-1}
@@ -875,7 +958,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
             CK(cudaGetLastError());
             g_launches++;
         }
-        s = spec_fixup(ctx, xd, Z, N, rg.off, fix_d, dc, de, trace ? ds : nullptr, st,
+        s = spec_fixup(ctx, xd, Z, N, rg.off, fix_d, dc, de, trace ? ds : nullptr, st, cfg.Rc,
                        smode == 1 ? sr->col_last : nullptr, cfg.ck ? sr : nullptr);
         if (s != SDTW_OK) return s;
     } else if (cfg.persistent) {
@@ -885,6 +968,11 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         g_launches++;
     }
     if (o.profile) CK(cudaEventRecord(ctx->ev1, st));
+    if ((cfg.half == 8 || cfg.half == 9) && !o.q8_int_out && !o.q8_codes_in) {   // sdtw_batch: normalised units
+        sdtw::q8_scale_kernel<<<(unsigned)((Z + 255) / 256), 256, 0, st>>>(dc, Z, q8_codebook_dev(ctx), ctx->flag_d);
+        CK(cudaGetLastError());
+        g_launches++;
+    }
     CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (o.profile) {
@@ -1241,6 +1329,9 @@ sdtw_status sdtw_set_reference(const float* Y, int64_t M) {
     if (*ctx->flag_h) { cudaFree(buf); return fail(SDTW_E_NONFINITE, "reference contains a non-finite sample"); }
     if (ctx->ref) cudaFree(ctx->ref);
     ctx->ref = buf;
+    if (ctx->ref_q8) cudaFree(ctx->ref_q8);          // uint8 codes: rebuilt for the new reference
+    ctx->ref_q8 = nullptr;
+    ctx->q8_clip = -1;
     ctx->M = M;
     ctx->Malloc = Malloc;
     ctx->ref_normalized = norm;
@@ -1353,6 +1444,71 @@ sdtw_status sdtw_path(const float* Q, int64_t n_queries, int64_t N, float* out_c
     return run_path(Q, n_queries, N, out_cost, out_end, out_start, path_lo, path_hi);
 }
 
+sdtw_status sdtw_batch_q8(const float* Q, int64_t n_queries, int64_t N, int32_t* out_cost, int64_t* out_end) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    const Options saved = g_opt;
+    g_opt.precision = 8;
+    g_opt.q8_int_out = 1;
+    // the integer cost travels as the fp32 bit pattern of the int32 through the pipeline
+    const sdtw_status s = run_batch(Q, n_queries, N, reinterpret_cast<float*>(out_cost), out_end, nullptr, false);
+    g_opt = saved;
+    return s;
+}
+
+sdtw_status sdtw_q8_codebook(float* lo, float* hi) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    Ctx* ctx;
+    sdtw_status s = get_ctx(&ctx);
+    if (s != SDTW_OK) return s;
+    if (!ctx->ref) return fail(SDTW_E_NOREF, "no reference set on this device");
+    s = ensure_q8(ctx, g_opt.stream);
+    if (s != SDTW_OK) return s;
+    if (lo) *lo = ctx->q8_lo;
+    if (hi) *hi = ctx->q8_hi;
+    return SDTW_OK;
+}
+
+sdtw_status sdtw_quantize(const float* in, int64_t n, uint8_t* out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (n < 0 || (n > 0 && (!in || !out))) return fail(SDTW_E_ARG, "n must be >= 0 and pointers non-NULL");
+    Ctx* ctx;
+    sdtw_status s = get_ctx(&ctx);
+    if (s != SDTW_OK) return s;
+    if (!ctx->ref) return fail(SDTW_E_NOREF, "no reference set on this device");
+    if (n == 0) return SDTW_OK;
+    cudaStream_t st = g_opt.stream;
+    s = ensure_q8(ctx, st);
+    if (s != SDTW_OK) return s;
+    const int ki = ptr_kind(in), ko = ptr_kind(out);
+    if (ki < 0 || ko < 0) return fail(SDTW_E_ARG, "device pointer on another device");
+    const float* id = in;
+    if (ki == 0) {
+        s = grow(&ctx->ws_q, &ctx->ws_q_n, (size_t)n);
+        if (s != SDTW_OK) return s;
+        CK(cudaMemcpyAsync(ctx->ws_q, in, (size_t)n * sizeof(float), cudaMemcpyHostToDevice, st));
+        id = ctx->ws_q;
+    }
+    unsigned char* od = out;
+    if (ko == 0) {
+        s = grow(&ctx->ws_out, &ctx->ws_out_n, (size_t)n);
+        if (s != SDTW_OK) return s;
+        od = ctx->ws_out;
+    }
+    CK(cudaMemsetAsync(ctx->flag_d, 0, sizeof(int), st));
+    sdtw::finite_check_kernel<<<4 * ctx->sms, 256, 0, st>>>(id, n, ctx->flag_d);
+    sdtw::q8_codes_u8_kernel<<<4 * ctx->sms, 256, 0, st>>>(id, n, q8_codebook_dev(ctx), od);
+    g_launches += 2;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (*ctx->flag_h) return fail(SDTW_E_NONFINITE, "input contains a non-finite sample");
+    if (ko == 0) {
+        CK(cudaMemcpyAsync(out, od, (size_t)n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    return SDTW_OK;
+}
+
 sdtw_status sdtw_znormalize(const float* in, int64_t n_series, int64_t len, float* out) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (n_series < 0 || len < 1) return fail(SDTW_E_ARG, "len must be >= 1 and n_series >= 0");
@@ -1414,7 +1570,9 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_SCHED: if (v < 0 || v > 3) break; g_opt.sched = (int)v; return SDTW_OK;
         case SDTW_OPT_SEGMENTS: if (v < 0 || v > 4096) break; g_opt.segments = (int)v; return SDTW_OK;
         case SDTW_OPT_WORKERS: if (v < 0 || v > 32) break; g_opt.workers = (int)v; return SDTW_OK;
-        case SDTW_OPT_PRECISION: if (v != 16 && v != 32) break; g_opt.precision = (int)v; return SDTW_OK;
+        case SDTW_OPT_PRECISION: if (v != 8 && v != 16 && v != 32) break; g_opt.precision = (int)v; return SDTW_OK;
+        case SDTW_OPT_Q8_PRUNE: if (v < -1 || v > 255) break; g_opt.q8_prune = (int)v; return SDTW_OK;
+        case SDTW_OPT_Q8_CLIP: if (v < 0 || v >= 500000) break; g_opt.q8_clip = (int)v; return SDTW_OK;
         case SDTW_OPT_PAD: if (v < 0 || v > (1 << 20)) break; g_opt.pad = (int)v; return SDTW_OK;
         case SDTW_OPT_SPEC_ROUNDS: if (v < 0 || v > 4096) break; g_opt.spec_rounds = (int)v; return SDTW_OK;
         case SDTW_OPT_START: if (v < 0 || v > 2) break; g_opt.start = (int)v; return SDTW_OK;
@@ -1441,6 +1599,8 @@ sdtw_status sdtw_get_option(int key, int64_t* v) {
         case SDTW_OPT_SEGMENTS: *v = g_opt.segments; return SDTW_OK;
         case SDTW_OPT_WORKERS: *v = g_opt.workers; return SDTW_OK;
         case SDTW_OPT_PRECISION: *v = g_opt.precision; return SDTW_OK;
+        case SDTW_OPT_Q8_PRUNE: *v = g_opt.q8_prune; return SDTW_OK;
+        case SDTW_OPT_Q8_CLIP: *v = g_opt.q8_clip; return SDTW_OK;
         case SDTW_OPT_PAD: *v = g_opt.pad; return SDTW_OK;
         case SDTW_OPT_SPEC_ROUNDS: *v = g_opt.spec_rounds; return SDTW_OK;
         case SDTW_OPT_START: *v = g_opt.start; return SDTW_OK;
@@ -1495,6 +1655,9 @@ void sdtw_release(void) {
     cudaFree(c.ws_ckc);
     cudaFree(c.ws_win);
     cudaFree(c.ws_start);
+    cudaFree(c.ref_q8);
+    cudaFree(c.q8_ws);
+    cudaFree(c.ws_xq);
     cudaFree(c.flag_d);
     cudaFreeHost(c.flag_h);
     cudaEventDestroy(c.ev0);

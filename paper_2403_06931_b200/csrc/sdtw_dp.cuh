@@ -121,6 +121,7 @@ struct DpParams {
     float* ckpt;
     float* ckpt_c;
     int ck_sg, ck_rc;
+    int q8_tau2;           // uint8-codebook kernels with INF pruning: tau^2 (sdtw_q8.cuh)
 };
 
 template <bool TRACE> struct Entry { float d; };

@@ -13,6 +13,7 @@ DpKernel pick_dp_c4t(int WC, bool fma, bool cl);
 DpKernel pick_dpq_c1(int WC, bool fma, bool trace);
 DpKernel pick_dpq_c2(int WC, bool fma, bool trace);
 DpKernel pick_dp16(int WC);
+DpKernel pick_dp8(int WC, bool prune);      // uint8 codebook (sdtw_dp8.cu)
 DpKernel pick_dp_c2xs(int WC, bool fma);
 DpKernel pick_dp_c2ck(int WC, bool fma, bool xs);   // + round checkpoints (sdtw_dp_c2k.cu)
 inline DpKernel pick_dp(int C, int WC, bool fma, bool trace, bool cl) {

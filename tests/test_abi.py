@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared_symbols():
     hdr = open(os.path.join(ROOT, "include", "sdtw.h")).read()
-    return sorted(set(re.findall(r"\b(sdtw_[a-z_]+)\s*\(", hdr)))
+    return sorted(set(re.findall(r"\b(sdtw_[a-z0-9_]+)\s*\(", hdr)))
 
 
 def _builder():
