@@ -165,18 +165,21 @@ def _workload(cfg_name: str, rank: int, world: int, scaling: str):
                           cells_local=float(off[-1]) * M)
     Q = nanopore_queries(Zl, N, M, seed, first_query=first)
     if cfg.get("straddle"):
-        # every `every`-th query: a copy of the reference compressed `stride`x, placed 500..2,800
+        # every `every`-th query matches a `stride`x oversampled reference region placed 1,000
         # columns before a boundary of the 6-segment speculative plan (OPT_SEGMENTS=6 is set
-        # for this config; boundaries = floor(s*Pr/6) rounds x columns per round), so its match
-        # crosses the boundary for longer than the correction pass (2 rounds = 7,680 columns)
+        # for this config; boundary s = floor(s*Pr/6) rounds x columns per round), so its path
+        # runs N*stride - 1,000 columns past the boundary -- beyond the correction pass (2
+        # rounds = 7,680 columns at N = 2,000)
         import paper_2403_06931_b200 as sd
-        from datagen import straddle_queries
+        from datagen import straddle_workload
         every, stride = cfg["straddle"]
         cols = sd.round_columns(N)
         Pr = -(-M // cols)
+        bounds = [((s * Pr) // 6) * cols for s in range(1, 6)]
         ks = [k for k in range(Zl) if (first + k) % every == 0]
-        pos = [(((1 + j % 5) * Pr) // 6) * cols - 500 - 37 * (j // 5) for j in range(len(ks))]
-        Q[ks] = straddle_queries(Y, pos, N, stride, seed)
+        per = -(-len(ks) // len(bounds))
+        Y, Qs = straddle_workload(Y, bounds, per, N, stride, 1000, seed)
+        Q[ks] = Qs[:len(ks)]
     return Q, Y, dict(Z=Zg, Z_local=Zl, N=N, M=M, seed=seed, start=cfg["start"])
 
 

@@ -32,7 +32,7 @@ __all__ = [
     "cbf_reference",
     "cbf_batch",
     "embed_queries",
-    "straddle_queries",
+    "straddle_workload",
 ]
 
 # name -> (Z, N, M, seed, traceback)
@@ -47,8 +47,8 @@ CONFIGS = {
     "c5_8000": dict(Z=512, N=8000, M=1_000_000, seed=5, start=True),
     # the paper's generator family (CBF) at config-2 shape: throughput is data-oblivious
     "c2_cbf": dict(Z=512, N=2000, M=100_000, seed=2, start=False, cbf=True),
-    # config 3 with 1/8 of the queries replaced by compressed copies of the reference that
-    # straddle the speculative segment boundaries (the schedule's worst case)
+    # config 3 with 1/8 of the queries matching oversampled reference regions that straddle
+    # the speculative segment boundaries (the schedule's worst case)
     "c3_straddle": dict(Z=512, N=2000, M=10_000_000, seed=3, start=False, straddle=(8, 5)),
     # NEXT-4: a ragged batch of reads, lengths log-uniform in [500, 8000] (N = mean, info only)
     "c6_ragged": dict(Z=512, N=2700, M=1_000_000, seed=6, start=False, ragged=(500, 8000)),
@@ -189,13 +189,20 @@ def embed_queries(Y: np.ndarray, Z: int, N: int, seed: int, stretch: int = 1):
     return Q, starts.astype(np.int64)
 
 
-def straddle_queries(Y: np.ndarray, positions, N: int, stride: int, seed: int) -> np.ndarray:
-    """Queries that are compressed copies of the reference: query k = Y[p_k + stride*i] for
-    i < N (every stride-th sample, so the warp path spans N*stride reference columns) plus
-    Gaussian noise of 0.2 level units -- the adversarial case of the speculative schedule
-    when p_k sits just before a segment boundary (bench config c3_straddle)."""
+def straddle_workload(Y: np.ndarray, boundaries, Z_per: int, N: int, stride: int, lead: int, seed: int):
+    """The speculative schedule's adversarial case: around each boundary b
+    the reference is replaced on [b - lead, b - lead + N*stride) by a `stride`x oversampled
+    level sequence L (each of N levels held `stride` samples, as in a slow-translocation /
+    repeat region), and Z_per queries per boundary are L plus Gaussian noise (0.2 level
+    units).  Their optimal paths start before b and run N*stride - lead columns past it.
+    Returns (Y', Q[len(boundaries)*Z_per, N])."""
     rng = _rng(seed, 9)
-    out = np.empty((len(positions), N), np.float32)
-    for k, p in enumerate(positions):
-        out[k] = Y[int(p):int(p) + N * stride:stride] + 0.2 * rng.standard_normal(N)
-    return out.astype(np.float32)
+    Y = np.array(Y, dtype=np.float32, copy=True)
+    qs = []
+    for b in boundaries:
+        p = int(b) - lead
+        L = Y[p:p + N].copy()
+        Y[p:p + N * stride] = np.repeat(L, stride)
+        for _ in range(Z_per):
+            qs.append(L + 0.2 * rng.standard_normal(N))
+    return Y, np.stack(qs).astype(np.float32)

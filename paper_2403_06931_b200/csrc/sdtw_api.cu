@@ -530,6 +530,9 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
 // Speculative segments: queries whose correction pass was not overtaken within Rc rounds
 // (fix[q] != 0) are recomputed with sequential segments from their normalised rows and
 // their results replace the speculative ones.
+#ifndef SDTW_FIXUP_SEQ
+#define SDTW_FIXUP_SEQ 0    // A/B only: 1 recomputes failed queries with one CTA each (the r01 fixup)
+#endif
 sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const std::vector<int64_t>* off,
                        const int* fix_d, float* dc, int64_t* de, int64_t* ds, cudaStream_t st, int Rc,
                        float* col_last = nullptr, const SegReq* ckr = nullptr) {
@@ -604,10 +607,12 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
         // ~1.4 s per 10M-sample query, a cliff on top of a 1.2 s batch).  Queries that fail
         // again recurse with 16 Rc, ...; once the corrections no longer fit (Pr < 4(Rc+1))
         // the plan falls back to sequential segments, so the recursion ends.
+#if !SDTW_FIXUP_SEQ
         g_opt.sched = 0;
         g_opt.spec_rounds = 4 * std::max(Rc, 1);
         g_opt.segments = 0;
         g_opt.workers = 0;
+#endif
         s = run_batch(rows, F, off ? nmax2 : N, fc, fe, ds ? fs : nullptr, ds != nullptr, nullptr, rg2);
     }
     g_opt = saved;
