@@ -217,8 +217,9 @@ sdtw_status sdtw_merge_candidates(const float* cost, const int64_t* end, const i
  * exact integer cost: out_cost[q] = min_j D(N-1, j) over the integer recurrence
  *     D(i,j) = INF                                    if |cx_i - cy_j| > tau (pruning on)
  *            = min((cx_i - cy_j)^2 + min(D(i-1,j), D(i,j-1), D(i-1,j-1)), INF)   otherwise,
- * INF = 2^30 (a cost of INF: every path crosses a pruned cell); out_end[q] = smallest argmin.
- * Queries are z-normalised first when SDTW_OPT_NORMALIZE=1, then coded.  N <= 12,000.
+ * INF = 2^30 (a cost of INF: every path crosses a pruned cell; out_end = 0 then);
+ * out_end[q] = smallest argmin.  Queries are z-normalised first when SDTW_OPT_NORMALIZE=1,
+ * then coded.  N <= 12,000 (<= 8,000 with pruning).
  * Pointers host or device.  Errors: as sdtw_batch, SDTW_E_ARG for N > 12,000. */
 sdtw_status sdtw_q8_codebook(float* lo, float* hi);
 sdtw_status sdtw_quantize(const float* in, int64_t n, uint8_t* out);

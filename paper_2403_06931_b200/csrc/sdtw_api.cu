@@ -210,6 +210,8 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     if (half && trace) return fail(SDTW_E_ARG, "the packed-half and uint8 precisions have no start index (OPT_PRECISION=32)");
     if (half && o.cluster > 1) return fail(SDTW_E_ARG, "the packed-half and uint8 precisions run without clusters");
     if (half && half != 16 && N > sdtw::kQ8MaxN) return fail(SDTW_E_ARG, "the uint8 precision takes queries of <= 12,000 samples");
+    if (half == 9 && N > sdtw::kQ8PruneMaxN)
+        return fail(SDTW_E_ARG, "the uint8 precision with INF pruning takes queries of <= 8,000 samples");
     const int packed = half ? 1 : (o.packed < 0 ? (trace ? 0 : 1) : o.packed);
     const bool dual = packed >= 3;
     int C = dual ? (packed == 3 ? 2 : 1) : (packed == 0 ? 1 : (packed == 1 ? 2 : 4));
@@ -947,12 +949,15 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         CK(cudaGetLastError());
         g_launches++;
         if (smode == 1) {                                   // free-DP columns of kinds A_0 and B_{Sg-1}
+            // (copied only when no sample was non-finite: no partial results on error)
+            CK(cudaMemcpyAsync(ctx->flag_h, ctx->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
             const size_t pitch = (size_t)cfg.S * cfg.Pd * sizeof(float);
             const float* bg = static_cast<const float*>(p.bnd_g);
-            if (sr->col_check)
+            if (sr->col_check && !*ctx->flag_h)
                 CK(cudaMemcpy2DAsync(sr->col_check, (size_t)N * 4, bg, pitch, (size_t)N * 4, (size_t)Z,
                                      cudaMemcpyDeviceToDevice, st));
-            if (sr->col_last)
+            if (sr->col_last && !*ctx->flag_h)
                 CK(cudaMemcpy2DAsync(sr->col_last, (size_t)N * 4, bg + (size_t)(2 * cfg.Sseg - 1) * cfg.Pd, pitch,
                                      (size_t)N * 4, (size_t)Z, cudaMemcpyDeviceToDevice, st));
             if (sr->check_cols) *sr->check_cols = (int64_t)cfg.Rc * 32LL * cfg.C * cfg.GW * cfg.WC;
@@ -973,6 +978,11 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         g_launches++;
     }
     if (o.profile) CK(cudaEventRecord(ctx->ev1, st));
+    if (cfg.half == 9 && !o.q8_codes_in) {              // pruning: (>= 2^29) -> (INF, end 0)
+        sdtw::q8_canon_kernel<<<(unsigned)((Z + 255) / 256), 256, 0, st>>>(dc, de, Z, ctx->flag_d);
+        CK(cudaGetLastError());
+        g_launches++;
+    }
     if ((cfg.half == 8 || cfg.half == 9) && !o.q8_int_out && !o.q8_codes_in) {   // sdtw_batch: normalised units
         sdtw::q8_scale_kernel<<<(unsigned)((Z + 255) / 256), 256, 0, st>>>(dc, Z, q8_codebook_dev(ctx), ctx->flag_d);
         CK(cudaGetLastError());

@@ -1298,7 +1298,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
             for (int r = threadIdx.x; r < Pd; r += blockDim.x) bo[r] = bnd[r];
         }
         if constexpr (BDP) {
-            if (spec && P.col_out)
+            if (spec && P.col_out && *P.err_flag == 0)       // no partial results on error
                 for (int r = threadIdx.x; r < N; r += blockDim.x) P.col_out[(long)q * N + r] = bnd[r].d;
         }
         __syncthreads();

@@ -16,7 +16,8 @@
 //    D = min(d + m, INF), m = min(diag, up, left), INF = 2^30 (> every finite cost: N <=
 //    12,000 rows x 255^2).  Without pruning (tau >= 255) the clamp never binds on the true
 //    DP (every cell has a finite vertical path from its own free start), so the kernel omits
-//    it: VIMNMX3 + IADD + IMAD per cell.
+//    it: VIMNMX3 + IADD + IMAD per cell.  With pruning the kernel computes an equivalent
+//    unclamped form (kQ8Pruned below) and canonicalises the result.
 //
 // GPU side: the codebook is two exact order statistics found by a two-pass radix select
 // (16 + 16 bits of the order-preserving key of the fp32 sample) over the reference buffer;
@@ -31,6 +32,15 @@ namespace sdtw {
 
 constexpr int kQ8Inf = 1 << 30;
 constexpr int kQ8MaxN = 12000;
+// INF pruning on the GPU: a pruned cell takes kQ8Pruned = 2^29 and the others d + m without a
+// clamp (5 SASS instead of a 6-SASS select + VIADDMNMX clamp, and balanced 3 ALU / 3 FMA-pipe).
+// With N <= 8,000 every path that avoids pruned cells costs <= 8,000 x 255^2 < 2^29, so a
+// cell's value is < 2^29 exactly when the oracle's clamped value (G20/G21) is finite, and then
+// the two are equal; every true value on rows < N stays < 2^29 + 8,000 x 255^2 < 2^30 = the
+// boundary INF (the speculative decomposition needs INF above every true boundary value).
+// q8_canon_kernel maps a final cost >= 2^29 (every path pruned) to the oracle's (INF, end 0).
+constexpr int kQ8Pruned = 1 << 29;
+constexpr int kQ8PruneMaxN = 8000;
 
 struct I2 { int a, b; };   // one column of both chains
 
@@ -60,9 +70,10 @@ struct Q8Arith {
         if constexpr (!PRUNE) {
             return t * t + m;
         } else {
+            // pruned: the fixed value 2^29 (not INF + m: no growth along pruned chains), else
+            // d + m unclamped -- see kQ8Pruned; the host canonicalises costs >= 2^29 to INF
             const int d = t * t;
-            const unsigned dd = d > tau2 ? (unsigned)kQ8Inf : (unsigned)d;
-            return (int)__viaddmin_u32(dd, (unsigned)m, (unsigned)kQ8Inf);
+            return d > tau2 ? kQ8Pruned : d + m;
         }
     }
     __device__ static __forceinline__ V cell(V dg, V up, V left, V xx, V y, int tau2) {
@@ -193,6 +204,16 @@ static __global__ void __launch_bounds__(256) q8_codes_u8_kernel(const float* __
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         out[i] = (unsigned char)q8_code(in[i], lo, hi);
+}
+
+// INF pruning: a cost >= kQ8Pruned means every path crosses a pruned cell -> (INF, end 0)
+static __global__ void q8_canon_kernel(float* cost, int64_t* end, int64_t n, const int* err) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || *err) return;
+    if (__float_as_int(cost[i]) >= kQ8Pruned) {
+        cost[i] = __int_as_float(kQ8Inf);
+        end[i] = 0;
+    }
 }
 
 // sdtw_batch at OPT_PRECISION=8: the integer cost (carried as fp32 bits) scaled back to

@@ -74,7 +74,7 @@ def test_config3_headline_vs_full_reference_oracle():
         assert _tie_ok(Qn[k], Yn, e[idx][k], ref["cost"][k]), (idx[k], e[idx][k], ref["end"][k])
 
 
-@pytest.mark.parametrize("name,step", [("c5_4000", 32), ("c5_8000", 64)])
+@pytest.mark.parametrize("name,step", [("c5_500", 16), ("c5_1000", 16), ("c5_4000", 32), ("c5_8000", 64)])
 def test_config5_start_index_vs_full_reference_oracle(brute_lib, name, step):
     Q, Y, (c, e, s) = _bench_launch(name, trace=True)
     idx = np.arange(0, Q.shape[0], step)
@@ -89,3 +89,39 @@ def test_config5_start_index_vs_full_reference_oracle(brute_lib, name, step):
             assert _tie_ok(Qn[k], Yn, e[q], ref["cost"][k]), (q, e[q], ref["end"][k])
         assert 0 <= s[q] <= e[q]
         assert _restricted(brute_lib, Qn[k], Yn, int(s[q]), int(e[q])) == c[q], q
+
+
+def test_config4_batch_on_one_gpu_vs_full_reference_oracle():
+    """Config 4's batch (4,096 x 2,000 vs 10M; 512 per GPU at 8 GPUs) in ONE launch on the
+    test GPU: 8 queries, one per 512-query rank shard, against the full-reference oracle."""
+    Q, Y, (c, e) = _bench_launch("c4", trace=False)
+    idx = np.arange(0, Q.shape[0], 512) + 37
+    Yn = oracle.znorm(Y[None])[0]
+    Qn = oracle.znorm(Q[idx])
+    ref = oracle.sdtw(Qn, Yn)
+    assert np.array_equal(c[idx].view(np.uint32), ref["cost"].view(np.uint32))
+    for k in np.nonzero(e[idx] != ref["end"])[0]:
+        assert _tie_ok(Qn[k], Yn, e[idx][k], ref["cost"][k])
+
+
+def test_config3_straddle_worst_case_vs_full_reference_oracle():
+    """The speculative schedule's adversarial workload (bench c3_straddle):
+    64 queries whose paths overrun the correction pass are recomputed (as their own
+    speculative batch); 8 of them and 4 benign queries against the full-reference oracle."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_bench", os.path.join(os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    with sd.options(OPT_SEGMENTS=6):
+        Q, Y, w = bench._workload("c3_straddle", 0, 1, "strong")
+        sd.set_reference(torch.as_tensor(Y, device=DEV))
+        c, e = [o.cpu().numpy() for o in sd.batch(torch.as_tensor(Q, device=DEV))]
+        assert sd.spec_recomputed() == 64
+    idx = np.array([0, 8, 64, 136, 256, 384, 448, 504, 1, 100, 301, 511])
+    Yn = oracle.znorm(Y[None])[0]
+    Qn = oracle.znorm(Q[idx])
+    ref = oracle.sdtw(Qn, Yn)
+    assert np.array_equal(c[idx].view(np.uint32), ref["cost"].view(np.uint32))
+    for k in np.nonzero(e[idx] != ref["end"])[0]:
+        assert _tie_ok(Qn[k], Yn, e[idx][k], ref["cost"][k])

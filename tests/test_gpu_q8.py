@@ -144,6 +144,16 @@ def test_q8_normalised_end_to_end_and_scaled_cost():
     assert np.array_equal(cf, want) and np.array_equal(ef, e)
 
 
+def test_q8_pruned_everywhere_and_long_queries():
+    """Every path pruned (cost INF, end 0 -- the GPU's unclamped form canonicalised) and the
+    longest pruned queries (N = 8,000) against the oracle's clamped definition."""
+    Q, Y = _inputs(6, 8000, 40_000, 60)
+    for tau in (0, 3, 60):
+        c, e = _gpu8(Q, Y, tau)
+        _check(Q, Y, c, e, tau)
+    assert np.all(_gpu8(Q, Y, 0)[0] == oracle.Q8_INF)
+
+
 def test_q8_ragged():
     rng = np.random.default_rng(59)
     lens = rng.integers(20, 600, 12)
@@ -168,6 +178,9 @@ def test_q8_errors():
             sd.traceback(np.ones((2, 10), np.float32))
         with pytest.raises(sd.SdtwError):
             sd.batch_q8(np.ones((1, 12_001), np.float32))
+        with sd.options(OPT_Q8_PRUNE=40):                     # pruning: N <= 8,000 (sdtw_q8.cuh)
+            with pytest.raises(sd.SdtwError):
+                sd.batch_q8(np.ones((1, 8_001), np.float32))
         with pytest.raises(sd.SdtwError):
             sd.quantize(np.array([1.0, np.nan], np.float32))
         with sd.options(OPT_SEGMENT_W=62):                   # W = 30 only

@@ -145,3 +145,35 @@ def test_reference_split_normalises_raw_inputs():
     sd.set_reference(torch.as_tensor(Y, device="cuda"))
     c, e = sd.batch(Q)
     assert np.array_equal(cost, c.cpu().numpy()) and np.array_equal(end, e.cpu().numpy()) and fb == 0
+
+
+def test_column_calls_write_nothing_on_nonfinite_input():
+    """ABI: no partial results on error -- a NaN query sample makes
+    sdtw_batch_columns / sdtw_boundary_dp return SDTW_E_NONFINITE with every output buffer
+    (cost, end, both columns / col_out) untouched."""
+    import ctypes
+    import oracle
+    import paper_2403_06931_b200 as sd
+    from datagen import nanopore_queries, nanopore_reference
+    M = 3840 * 20
+    Y = oracle.znorm(nanopore_reference(M, 75)[None])[0]
+    Q = torch.as_tensor(oracle.znorm(nanopore_queries(4, 300, M, 75)), device="cuda")
+    Q[2, 5] = float("nan")
+    with sd.options(OPT_NORMALIZE=0):
+        sd.set_reference(torch.as_tensor(Y, device="cuda"))
+        outs = [torch.full((4,), 7.0, device="cuda"), torch.full((4,), -3, dtype=torch.int64, device="cuda"),
+                torch.full((4, 300), 7.0, device="cuda"), torch.full((4, 300), 7.0, device="cuda")]
+        before = [o.clone() for o in outs]
+        n = ctypes.c_int64(0)
+        rc = sd._lib.sdtw_batch_columns(ctypes.c_void_p(Q.data_ptr()), 4, 300, ctypes.c_void_p(outs[0].data_ptr()),
+                                        ctypes.c_void_p(outs[1].data_ptr()), ctypes.c_void_p(outs[2].data_ptr()),
+                                        ctypes.c_void_p(outs[3].data_ptr()), ctypes.byref(n))
+        assert rc == sd.E_NONFINITE
+        bnd = torch.zeros((4, 300), device="cuda")
+        rc = sd._lib.sdtw_boundary_dp(ctypes.c_void_p(Q.data_ptr()), 4, 300, ctypes.c_void_p(bnd.data_ptr()), 0, 0,
+                                      ctypes.c_void_p(outs[0].data_ptr()), ctypes.c_void_p(outs[1].data_ptr()),
+                                      ctypes.c_void_p(outs[2].data_ptr()))
+        assert rc == sd.E_NONFINITE
+        torch.cuda.synchronize()
+    for a, b in zip(outs, before):
+        assert torch.equal(a, b)
