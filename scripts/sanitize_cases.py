@@ -25,5 +25,20 @@ with sd.options(OPT_SCHED=3, OPT_LANES=1):
     sd.batch_ragged(Qt.reshape(-1)[:900], off, start=True)
 with sd.options(OPT_PRECISION=16, OPT_SCHED=3, OPT_LANES=1):
     sd.batch(Qt)
+# round 2: uint8 codebook (radix-select codebook, quantiser, integer DP with / without pruning),
+# checkpointed start index (the traceback default) and its forced form, the reference-split calls
+for tau in (-1, 40):
+    with sd.options(OPT_Q8_PRUNE=tau, OPT_SCHED=3, OPT_LANES=1):
+        sd.batch_q8(Qt)
+    with sd.options(OPT_Q8_PRUNE=tau):
+        sd.batch_q8(Qt)
+sd.quantize(Qt)
+with sd.options(OPT_START=2):
+    sd.traceback(Qt)
+    sd.path(Qt[:2])
+with sd.options(OPT_LANES=1):
+    c, e, ck, cl, n = sd.batch_columns(Qt, last=False)
+    sd.boundary_dp(Qt, ck, False, n)
+    sd.columns_dominate(ck, ck)
 torch.cuda.synchronize()
 print("sanitize cases done")
