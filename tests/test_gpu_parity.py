@@ -303,3 +303,24 @@ def test_cbf_inputs_bit_exact():
     Y = oracle.znorm(cbf_reference(8000, 2)[None])[0]
     Q = oracle.znorm(cbf_batch(6, 256, 2))
     _check_exact(Q, Y, _gpu(Q, Y, trace=True), trace=True)
+
+
+def test_max_size_reference_exact_match_at_the_far_end():
+    """Maximum sizes: a 1.5e9-sample reference (6 GB, step and column counters near the int32
+    limit of the kernel's planning) -- queries cut verbatim from the far end and from the start
+    must score exactly 0 at their own end column (a property that holds at any size; raw mode),
+    and a length past the ABI limit is rejected before anything is allocated."""
+    M = 1_500_000_000
+    rng = np.random.default_rng(77)
+    Y = rng.standard_normal(M, dtype=np.float32)
+    starts = [M - 64, M - 1_000_003, 12_345, 1_073_741_800]       # incl. one across 2^30
+    Q = np.stack([Y[s:s + 64] for s in starts]).astype(np.float32)
+    with sd.options(OPT_NORMALIZE=0):
+        sd.set_reference(Y)
+        del Y
+        c, e = sd.batch(torch.as_tensor(Q, device=DEV))
+    assert torch.all(c == 0).item(), c
+    assert e.cpu().tolist() == [s + 63 for s in starts]
+    sd.release()
+    rc = sd._lib.sdtw_set_reference(ctypes.c_void_p(Q.ctypes.data), ctypes.c_int64(0x7fffffff))
+    assert rc == sd.E_ARG
