@@ -108,7 +108,7 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index):
         self.index = index
         self.samples = []
         self._stop = threading.Event()
@@ -120,8 +120,9 @@ class ClockSampler:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                row = [x.strip() for x in out.split(",")] if out else []
+                if len(row) >= 8:                   # skip error text / partial rows
+                    self.samples.append(row)
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -296,6 +297,9 @@ def main():
                     help="with --q8: INF-prune cells whose codes differ by more than TAU (-1: off)")
     ap.add_argument("--path", action="store_true",
                     help="step = sdtw_path (start index + full warp path, SURVEY NEXT-2)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 collective backend; gloo lets several ranks share one GPU (a functional "
+                         "check of the multi-rank path on a one-GPU box -- not a scaling number)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -310,13 +314,20 @@ def main():
 
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
     comm = None
+    tdev = dev                       # where the max-over-ranks reductions run
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+            tdev = torch.device("cpu")
         comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(), "rank": rank,
-                "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version())}
+                "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version()),
+                "ranks_per_gpu": max(1, -(-world // ndev))}
         print("[bench] communicator: %s world_size=%d rank=%d local_rank=%d device=%s nccl=%s"
               % (comm["backend"], comm["world_size"], rank, local, dev, comm["nccl_version"]),
               file=sys.stderr, flush=True)
@@ -365,7 +376,13 @@ def main():
     dp_ms = []
     recomputed = 0
     launches0 = sd.launch_count()
-    sampler = ClockSampler(local)
+    # nvidia-smi -i takes the physical index or the UUID; the UUID survives CUDA_VISIBLE_DEVICES
+    # remapping and several ranks sharing one GPU
+    try:
+        smi_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        smi_id = str(dev.index)
+    sampler = ClockSampler(smi_id)
     with sd.options(OPT_PROFILE=1), sampler:
         if world > 1:
             dist.barrier()
@@ -384,7 +401,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     cells_step = w["cells_local"] * world if ragged else float(w["Z"]) * N * M
@@ -463,7 +480,7 @@ def main():
             ts.append(e0.elapsed_time(e1) / 1e3)
         te = sum(ts)
         if world > 1:
-            t = torch.tensor([te], dtype=torch.float64, device=dev)
+            t = torch.tensor([te], dtype=torch.float64, device=tdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         e2e = {"value": cells_step * len(ts) / te / 1e9, "unit": "GCUPS",
