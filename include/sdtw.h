@@ -96,7 +96,8 @@ enum {
                                sdtw_batch returns cost x delta^2 (delta = (hi - lo)/255) in fp32,
                                sdtw_batch_q8 the exact integer cost; N <= 12,000.
                                16 and 8: sdtw_batch / sdtw_batch_ragged / sdtw_batch_q8 only
-                               (no start index), no clusters, OPT_PACKED ignored, W in {30, 62} */
+                               (no start index), no clusters, OPT_PACKED ignored; W in {14, 30
+                               (half default), 62} for 16, {14 (default), 30} for 8 */
     SDTW_OPT_Q8_PRUNE = 18, /* uint8 codebook: INF pruning of "far" cells: a cell with
                                |cx - cy| > tau is INF (2^30: no path through it); -1 (default)
                                or tau >= 255: off */

@@ -215,7 +215,9 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     const int packed = half ? 1 : (o.packed < 0 ? (trace ? 0 : 1) : o.packed);
     const bool dual = packed >= 3;
     int C = dual ? (packed == 3 ? 2 : 1) : (packed == 0 ? 1 : (packed == 1 ? 2 : 4));
-    int W = o.segment_w > 0 ? o.segment_w : (C == 4 ? 28 : (C == 2 ? 30 : 15));
+    // uint8 codebook: W = 14 (r02u sweep at config 3: 6.77 vs 6.32 TCUPS unpruned, 4.39 vs 2.60
+    // pruned -- the int32 chains' 30-column loop overflows the instruction footprint and spills)
+    int W = o.segment_w > 0 ? o.segment_w : (C == 4 ? 28 : (C == 2 ? ((half == 8 || half == 9) ? 14 : 30) : 15));
     if (W % C != 0) return fail(SDTW_E_ARG, "segment width must be a multiple of the chains per lane");
     int WC = W / C;
     if (!pick_kernel(C, WC, true, false, false, dual, half))

@@ -5,6 +5,7 @@
 namespace sdtw {
 DpKernel pick_dp16(int WC) {
     switch (WC) {
+        case 7: return sdtw_dp2_kernel<Half2Arith, 7>;
         case 15: return sdtw_dp2_kernel<Half2Arith, 15>;
         case 31: return sdtw_dp2_kernel<Half2Arith, 31>;
         default: return nullptr;

@@ -42,7 +42,7 @@ def _check(Q, Y, c, e, idx=None):
         assert ref["last_rows"][k, ee[k]] == ref["cost"][k], (k, ee[k], ref["end"][k])
 
 
-@pytest.mark.parametrize("W", [30, 62])
+@pytest.mark.parametrize("W", [14, 30, 62])
 @pytest.mark.parametrize("Z,N,M", [(8, 64, 4096), (5, 300, 2000), (3, 1, 500), (3, 40, 1), (3, 90, 60),
                                    (4, 257, 3000)])
 def test_half_bit_exact_small(Z, N, M, W):

@@ -82,12 +82,13 @@ def test_codes_bit_exact():
 
 
 # ------------------------------------------------------------------ DP parity
+@pytest.mark.parametrize("W", [14, 30])
 @pytest.mark.parametrize("tau", [-1, 0, 24, 96])
 @pytest.mark.parametrize("Z,N,M", [(8, 64, 4096), (5, 300, 2000), (3, 1, 500), (3, 40, 1), (3, 90, 60),
                                    (4, 257, 3001)])
-def test_q8_bit_exact_small(Z, N, M, tau):
+def test_q8_bit_exact_small(Z, N, M, tau, W):
     Q, Y = _inputs(Z, N, M, 50 + N)
-    c, e = _gpu8(Q, Y, tau)
+    c, e = _gpu8(Q, Y, tau, OPT_SEGMENT_W=W)
     _check(Q, Y, c, e, tau)
 
 
@@ -97,7 +98,8 @@ def test_q8_schedules_identical(tau):
     base = _gpu8(Q, Y, tau)
     _check(Q, Y, *base, tau)
     for opts in (dict(OPT_SCHED=1), dict(OPT_LANES=2), dict(OPT_LANES=8, OPT_CHUNK=32),
-                 dict(OPT_SCHED=2, OPT_SEGMENTS=3), dict(OPT_LANES=3), dict(OPT_SCHED=3)):
+                 dict(OPT_SCHED=2, OPT_SEGMENTS=3), dict(OPT_LANES=3), dict(OPT_SCHED=3),
+                 dict(OPT_SEGMENT_W=30), dict(OPT_SEGMENT_W=30, OPT_SCHED=2, OPT_SEGMENTS=3)):
         got = _gpu8(Q, Y, tau, **opts)
         assert np.array_equal(got[0], base[0]) and np.array_equal(got[1], base[1]), opts
 
@@ -183,7 +185,7 @@ def test_q8_errors():
                 sd.batch_q8(np.ones((1, 8_001), np.float32))
         with pytest.raises(sd.SdtwError):
             sd.quantize(np.array([1.0, np.nan], np.float32))
-        with sd.options(OPT_SEGMENT_W=62):                   # W = 30 only
+        with sd.options(OPT_SEGMENT_W=62):                   # W = 14 or 30
             with pytest.raises(sd.SdtwError):
                 sd.batch_q8(np.ones((1, 10), np.float32))
     with pytest.raises(sd.SdtwError):
