@@ -34,6 +34,7 @@ for cfg in configs:
             ref = (c.clone(), e.clone())
         else:
             same = bool(torch.equal(c, ref[0]) and torch.equal(e, ref[1]))
-        print(json.dumps(dict(cfg=cfg, ms=dt * 1e3, gcups=Z * N * M / dt / 1e9, identical=same)), flush=True)
+        print(json.dumps(dict(cfg=cfg, ms=dt * 1e3, gcups=Z * N * M / dt / 1e9, identical=same,
+                              recomputed=sd.spec_recomputed())), flush=True)
     except Exception as ex:
         print(json.dumps(dict(cfg=cfg, error=str(ex)[:200])), flush=True)
