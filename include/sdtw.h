@@ -101,10 +101,14 @@ enum {
     SDTW_OPT_Q8_PRUNE = 18, /* uint8 codebook: INF pruning of "far" cells: a cell with
                                |cx - cy| > tau is INF (2^30: no path through it); -1 (default)
                                or tau >= 255: off */
-    SDTW_OPT_Q8_CLIP = 19   /* uint8 codebook: tail mass clamped to each extreme code, in parts
+    SDTW_OPT_Q8_CLIP = 19,  /* uint8 codebook: tail mass clamped to each extreme code, in parts
                                per million of the reference (default 1000 = 0.1 %); the
                                codebook spans the order statistics of rank k and M-1-k,
                                k = floor(clip * (M-1) / 1e6) */
+    SDTW_OPT_STAT_FIXUP_DEPTH = 20 /* read-only (sdtw_get_option): how many levels of speculative
+                               recomputation the last call on this device needed (0: none; 1:
+                               failed queries re-run once as their own speculative batch with
+                               corrections x4; 2: some of those failed again; ...) */
 };
 
 /* Install the reference Y[M] on the current device (copied into a

@@ -68,8 +68,14 @@ struct Ctx {
     unsigned char* ws_rag = nullptr; size_t ws_rag_n = 0;       // ragged-batch offsets + lengths
     int* order_d = nullptr; size_t order_n = 0;     // unit grab order (device) and its key
     int4* utab_d = nullptr; size_t utab_n = 0;      // speculative segments: unit-kind table
-    float* ws_fix = nullptr; size_t ws_fix_n = 0;   // speculative segments: recomputed queries
-    float* ws_fixck = nullptr; size_t ws_fixck_n = 0;   // their round checkpoints
+    // speculative segments: recomputed queries and their round checkpoints, one workspace per
+    // recursion depth (a recomputation runs the speculative schedule again and may recompute
+    // some of ITS queries: the inner level must not overwrite the outer level's rows/results)
+    static constexpr int kFixDepth = 8;
+    float* ws_fix[kFixDepth] = {};  size_t ws_fix_n[kFixDepth] = {};
+    float* ws_fixck[kFixDepth] = {}; size_t ws_fixck_n[kFixDepth] = {};
+    int fix_depth = 0;
+    int last_fix_depth = 0;                         // deepest recomputation level of the last call
     float* ws_ck = nullptr; size_t ws_ck_n = 0;     // round checkpoints [Z][Pr][Pd] (checkpointed start index)
     float* ws_ckc = nullptr; size_t ws_ckc_n = 0;   // speculative correction units' checkpoints
     unsigned char* ws_win = nullptr; size_t ws_win_n = 0;   // start windows: codes, rows, query lists
@@ -560,11 +566,13 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
         nmax2 = std::max(nmax2, n);
     }
     const size_t need = 5 * (size_t)F + (size_t)off2[F] * (col_last ? 2 : 1);   // (end, start, cost) + rows (+ columns)
-    sdtw_status s = grow(&ctx->ws_fix, &ctx->ws_fix_n, need);
+    const int depth = ctx->fix_depth;
+    if (depth >= Ctx::kFixDepth) return fail(SDTW_E_CUDA, "internal: speculative recomputation nested too deep");
+    sdtw_status s = grow(&ctx->ws_fix[depth], &ctx->ws_fix_n[depth], need);
     if (s != SDTW_OK) return s;
-    int64_t* fe = reinterpret_cast<int64_t*>(ctx->ws_fix);
+    int64_t* fe = reinterpret_cast<int64_t*>(ctx->ws_fix[depth]);
     int64_t* fs = fe + F;
-    float* fc = ctx->ws_fix + 4 * F;
+    float* fc = ctx->ws_fix[depth] + 4 * F;
     float* rows = fc + F;
     for (int64_t k = 0; k < F; ++k) {
         const int64_t src = off ? (*off)[idx[k]] : idx[k] * N;
@@ -580,24 +588,35 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
     g_opt.normalize = 0;
     g_opt.profile = 0;
     g_opt.q8_codes_in = 1;                            // uint8 codebook: rows are codes already
-    g_opt.sched = 1;                                  // one CTA per ring: no speculation again
+    g_opt.sched = 1;                                  // one CTA per ring (the column-returning paths)
     g_opt.stream = st;
     const int64_t fixed_before = F;
+    ++ctx->fix_depth;                                 // nested recomputations use the next workspace
+    ctx->last_fix_depth = std::max(ctx->last_fix_depth, ctx->fix_depth);
     float* fcol = rows + off2[F];
     float* fck = nullptr;
     if (ckr) {                                        // round checkpoints of the recomputed queries
         const size_t per = (size_t)ckr->ck_Pr * ckr->ck_Pd;
-        s = grow(&ctx->ws_fixck, &ctx->ws_fixck_n, (size_t)F * per);
+        s = grow(&ctx->ws_fixck[depth], &ctx->ws_fixck_n[depth], (size_t)F * per);
         if (s == SDTW_OK) {
-            fck = ctx->ws_fixck;
+            fck = ctx->ws_fixck[depth];
             SegReq r3 = *ckr;
             r3.ck = fck;
+#if !SDTW_FIXUP_SEQ
+            // as below: the recomputed queries as their own speculative batch, corrections x4
+            // (the checkpoint layout depends only on N and the ring, not on the schedule)
+            g_opt.sched = 0;
+            g_opt.spec_rounds = 4 * std::max(Rc, 1);
+            g_opt.segments = 0;
+            g_opt.workers = 0;
+#endif
             s = run_batch(rows, F, N, fc, fe, nullptr, false, nullptr, Ragged(), &r3);
         }
-        if (s == SDTW_OK)
-            for (int64_t k = 0; k < F; ++k)
-                CK(cudaMemcpyAsync(ckr->ck + idx[k] * per, fck + k * per, per * sizeof(float), cudaMemcpyDeviceToDevice,
-                                   st));
+        for (int64_t k = 0; s == SDTW_OK && k < F; ++k) {   // (no early return: options restored below)
+            const cudaError_t e = cudaMemcpyAsync(ckr->ck + idx[k] * per, fck + k * per, per * sizeof(float),
+                                                  cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync(recomputed checkpoints)");
+        }
     } else if (col_last) {                            // also the true last column: one-unit DP per query
         g_opt.sched = 3;
         SegReq r2;
@@ -620,6 +639,7 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
         s = run_batch(rows, F, off ? nmax2 : N, fc, fe, ds ? fs : nullptr, ds != nullptr, nullptr, rg2);
     }
     g_opt = saved;
+    --ctx->fix_depth;
     if (s != SDTW_OK) return s;
     if (col_last)
         for (int64_t k = 0; k < F; ++k)
@@ -867,6 +887,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     }
     int* fix_d = nullptr;
     ctx->last_fixups = 0;
+    if (ctx->fix_depth == 0) ctx->last_fix_depth = 0;
     if (cfg.persistent) {
         const size_t ent = cfg.half == 16 ? 2 : (trace ? 8 : 4) * (cfg.dual ? 2 : 1);
         const size_t R = (size_t)cfg.units;
@@ -1618,6 +1639,13 @@ sdtw_status sdtw_get_option(int key, int64_t* v) {
         case SDTW_OPT_PRECISION: *v = g_opt.precision; return SDTW_OK;
         case SDTW_OPT_Q8_PRUNE: *v = g_opt.q8_prune; return SDTW_OK;
         case SDTW_OPT_Q8_CLIP: *v = g_opt.q8_clip; return SDTW_OK;
+        case SDTW_OPT_STAT_FIXUP_DEPTH: {
+            Ctx* ctx;
+            const sdtw_status s = get_ctx(&ctx);
+            if (s != SDTW_OK) return s;
+            *v = ctx->last_fix_depth;
+            return SDTW_OK;
+        }
         case SDTW_OPT_PAD: *v = g_opt.pad; return SDTW_OK;
         case SDTW_OPT_SPEC_ROUNDS: *v = g_opt.spec_rounds; return SDTW_OK;
         case SDTW_OPT_START: *v = g_opt.start; return SDTW_OK;
@@ -1666,8 +1694,10 @@ void sdtw_release(void) {
     cudaFree(c.ws_rag);
     cudaFree(c.order_d);
     cudaFree(c.utab_d);
-    cudaFree(c.ws_fix);
-    cudaFree(c.ws_fixck);
+    for (int k = 0; k < Ctx::kFixDepth; ++k) {
+        cudaFree(c.ws_fix[k]);
+        cudaFree(c.ws_fixck[k]);
+    }
     cudaFree(c.ws_ck);
     cudaFree(c.ws_ckc);
     cudaFree(c.ws_win);

@@ -194,3 +194,28 @@ def test_spec_edge_shapes_identical_to_sequential(Z, N, M, start):
     with sd.options(OPT_SCHED=2):
         b = [t.cpu() for t in run(Q)]
     assert all(torch.equal(x, y) for x, y in zip(a, b))
+
+
+def test_nested_recomputation_levels_are_exact():
+    """Failed queries are re-run as their own speculative batch with corrections x4 (DESIGN.md
+    §13); on a fully 5x-oversampled reference with one-round corrections some of THOSE fail
+    again (a second level, OPT_STAT_FIXUP_DEPTH = 2), each level in its own workspace --
+    cost, end and (checkpointed) start all exact against the oracle."""
+    import oracle
+    from datagen import nanopore_reference
+    M, N, Z, seed = 100_000, 1500, 12, 81
+    levels = oracle.znorm(nanopore_reference(M // 5 + 10, seed)[None])[0]
+    Y = np.repeat(levels, 5)[:M].astype(np.float32)
+    rng = np.random.default_rng(seed)
+    starts = rng.integers(0, M // 5 - N - 1, size=Z)
+    Q = np.stack([levels[s:s + N] + 0.05 * rng.standard_normal(N) for s in starts]).astype(np.float32)
+    ref = oracle.sdtw(Q, Y, start=True)
+    with sd.options(OPT_NORMALIZE=0, OPT_SCHED=3, OPT_LANES=1, OPT_SPEC_ROUNDS=1):
+        sd.set_reference(torch.as_tensor(Y, device="cuda"))
+        c, e = sd.batch(torch.as_tensor(Q, device="cuda"))
+        assert sd.spec_recomputed() == Z and sd.get_option(sd.OPT_STAT_FIXUP_DEPTH) >= 2
+        c2, e2, s2 = sd.traceback(torch.as_tensor(Q, device="cuda"))
+    for cc, ee in ((c, e), (c2, e2)):
+        assert np.array_equal(cc.cpu().numpy().view(np.uint32), ref["cost"].view(np.uint32))
+        assert np.array_equal(ee.cpu().numpy(), ref["end"])
+    assert np.array_equal(s2.cpu().numpy(), ref["start"])
