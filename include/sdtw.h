@@ -105,6 +105,12 @@ enum {
                                per million of the reference (default 1000 = 0.1 %); the
                                codebook spans the order statistics of rank k and M-1-k,
                                k = floor(clip * (M-1) / 1e6) */
+    SDTW_OPT_QUERY_ROWS = 21, /* where the DP kernel reads the query rows: 0 (default) auto --
+                               shared memory, or for long queries a global pair-layout buffer
+                               read through L1 when that keeps more CTAs resident; 1 shared
+                               memory; 2 global memory (two-chain fp32 cost/end kernels and the
+                               checkpointed start index; SDTW_E_ARG otherwise).  Results are
+                               identical */
     SDTW_OPT_STAT_FIXUP_DEPTH = 20 /* read-only (sdtw_get_option): how many levels of speculative
                                recomputation the last call on this device needed (0: none; 1:
                                failed queries re-run once as their own speculative batch with

@@ -71,7 +71,7 @@ for _n in ("sdtw_set_reference", "sdtw_batch", "sdtw_batch_ragged", "sdtw_traceb
 OK, E_ARG, E_NOREF, E_CUDA, E_NOMEM, E_NONFINITE = range(6)
 OPT_NORMALIZE, OPT_FMA, OPT_SEGMENT_W, OPT_LANES, OPT_CLUSTER, OPT_STREAM, OPT_PACKED, OPT_CHUNK, \
     OPT_PROFILE, OPT_RING, OPT_SCHED, OPT_SEGMENTS, OPT_WORKERS, OPT_PRECISION, OPT_PAD, \
-    OPT_SPEC_ROUNDS, OPT_START, OPT_Q8_PRUNE, OPT_Q8_CLIP, OPT_STAT_FIXUP_DEPTH = range(1, 21)
+    OPT_SPEC_ROUNDS, OPT_START, OPT_Q8_PRUNE, OPT_Q8_CLIP, OPT_STAT_FIXUP_DEPTH, OPT_QUERY_ROWS = range(1, 22)
 _STATUS = {0: "SDTW_OK", 1: "SDTW_E_ARG", 2: "SDTW_E_NOREF", 3: "SDTW_E_CUDA", 4: "SDTW_E_NOMEM",
            5: "SDTW_E_NONFINITE"}
 

@@ -44,6 +44,7 @@ struct Options {
     int q8_clip = 1000;  // uint8 codebook: clipped tail mass per side, parts per million
     int q8_codes_in = 0; // (internal) the batch already holds codes (speculative recomputation)
     int q8_int_out = 0;  // (internal) sdtw_batch_q8: leave the integer costs
+    int query_rows = 0;  // 0 auto, 1 shared memory, 2 global memory (two-chain fp32 cost/end kernels)
     int pad = 0;         // extra idle rows per round period (0 = auto)
     int spec_rounds = 0; // speculative segments: rounds per correction pass (0 = auto)
     int start = 0;       // start index: 0 auto, 1 forward propagation, 2 checkpoints + walk-back
@@ -91,6 +92,7 @@ struct Ctx {
     int q8_clip = -1;                               // clip of the current codes (-1: none built)
     float q8_lo = 0.f, q8_hi = 0.f;
     float* ws_xq = nullptr;  size_t ws_xq_n = 0;    // query codes
+    float* ws_xg = nullptr;  size_t ws_xg_n = 0;    // query rows in the global pair layout (XG kernels)
     int* flag_d = nullptr;
     int* flag_h = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -168,12 +170,13 @@ using sdtw::DpKernel;
 // dual: the dual-query kernel (two queries per lane, C chains of scalar-y strips)
 // half: 0 fp32; 16 packed half; 8 / 9 uint8 codebook without / with INF pruning
 DpKernel pick_kernel(int C, int WC, bool fma, bool trace, bool cl, bool dual = false, int half = 0,
-                     bool xs = false) {
+                     int xs = 0) {
     if (half) {
         if (C != 2 || trace || cl || dual) return nullptr;
         return half == 16 ? sdtw::pick_dp16(WC) : sdtw::pick_dp8(WC, half == 9);
     }
-    if (xs) return (C == 2 && !trace && !cl && !dual) ? sdtw::pick_dp_c2xs(WC, fma) : nullptr;
+    if (xs) return (C == 2 && !trace && !cl && !dual) ? (xs == 2 ? sdtw::pick_dp_c2xg(WC, fma) : sdtw::pick_dp_c2xs(WC, fma))
+                                                      : nullptr;
     if (dual) {
         if (cl) return nullptr;
         return C == 1 ? sdtw::pick_dpq_c1(WC, fma, trace) : (C == 2 ? sdtw::pick_dpq_c2(WC, fma, trace) : nullptr);
@@ -188,7 +191,7 @@ struct LaunchCfg {
     int64_t units;   // rings per batch: queries, or query pairs when dual
     int need;        // V + (G+1)K: smallest ring-safe round period (ragged batches: per query)
     int half;        // two-chain reduced-precision kernel: 16 packed half, 8 / 9 uint8 codebook (9: INF pruning)
-    int xs;          // single-row query layout (long queries)
+    int xs;          // query rows: 0 shared-memory pairs, 1 single-row layout, 2 global memory (long queries)
     int spec = 0;    // speculative segments: Sseg segments, correction passes of Rc rounds
     int Sseg = 0, Rc = 0;
     int ck = 0;      // round checkpoints (the CKPT kernel)
@@ -299,14 +302,23 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
     // long queries: the single-row layout halves the rows' bytes; take it when that keeps
     // one more CTA resident (C == 2, cost/end, no cluster)
-    bool xs = false;
-    if (!half && !dual && !trace && C == 2 && CL == 1 && pick_kernel(C, WC, true, false, false, false, false, true)) {
+    // Even longer: the rows in global memory (read through L1: a warp's lanes sweep a window of
+    // a few hundred rows, so they stay L1-resident), the CTA keeps only the rings -- taken when
+    // that allows more resident CTAs than either shared-memory layout (up to the register
+    // limit of 4), or when forced by SDTW_OPT_QUERY_ROWS.
+    int xs = 0;
+    const bool xs_ok = !half && !dual && !trace && C == 2 && CL == 1;
+    if (xs_ok && o.query_rows != 1 && pick_kernel(C, WC, true, false, false, false, 0, 1)) {
         auto ctas = [&](int bytes) { return (int)((228 * 1024) / (bytes + 1024)); };
         const sdtw::SmemLayout Lx = sdtw::smem_layout(C, WC, trace, GW, (int)Pd, RS, true);
-        if (ctas(L.bytes) < 3 && ctas(Lx.bytes) > ctas(L.bytes)) { L = Lx; xs = true; }
+        if (ctas(L.bytes) < 3 && ctas(Lx.bytes) > ctas(L.bytes)) { L = Lx; xs = 1; }
+        const sdtw::SmemLayout Lg = sdtw::smem_layout(C, WC, trace, GW, (int)Pd, RS, false, true);
+        if (o.query_rows == 2 || (ctas(L.bytes) < 4 && std::min(ctas(Lg.bytes), 4) > ctas(L.bytes))) { L = Lg; xs = 2; }
+    } else if (o.query_rows == 2) {
+        return fail(SDTW_E_ARG, "query rows in global memory need the two-chain fp32 cost/end kernel (no clusters)");
     }
     *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0, dual ? 1 : 0, units, (int)need,
-                     half, xs ? 1 : 0};
+                     half, xs};
     // Persistent scheduling (default when a cluster is not requested): k resident CTAs
     // per SM, k = min(occupancy, rings / SMs), pull (ring, round-segment) units, so every
     // SM carries the same load whatever the batch size mod #SMs is.
@@ -380,8 +392,8 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
 }
 
 sdtw_status launch_dp(const LaunchCfg& c, bool fma, bool trace, const DpParams& p, cudaStream_t st) {
-    DpKernel k = c.ck ? sdtw::pick_dp_c2ck(c.WC, fma, c.xs != 0)
-                      : pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0, c.half, c.xs != 0);
+    DpKernel k = c.ck ? sdtw::pick_dp_c2ck(c.WC, fma, c.xs)
+                      : pick_kernel(c.C, c.WC, fma, trace, c.CL > 1, c.dual != 0, c.half, c.xs);
     if (!k) return fail(SDTW_E_ARG, "no kernel for this configuration");
     CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem));
     if (c.CL > 8) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -844,6 +856,15 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.X = xd;
     p.Y = (cfg.half == 8 || cfg.half == 9) ? ctx->ref_q8 : ctx->ref;
     p.q8_tau2 = cfg.half == 9 ? o.q8_prune * o.q8_prune : 0;
+    p.xg = nullptr;
+    if (cfg.xs == 2) {                                  // long queries: rows in global memory
+        s = grow(&ctx->ws_xg, &ctx->ws_xg_n, (size_t)Z * cfg.Pd * 2);
+        if (s != SDTW_OK) return s;
+        sdtw::xg_layout_kernel<<<(unsigned)Z, 256, 0, st>>>(xd, (int)N, cfg.Pd, cfg.need, qoff_d, qlen_d, ctx->ws_xg);
+        CK(cudaGetLastError());
+        g_launches++;
+        p.xg = ctx->ws_xg;
+    }
     p.Malloc = (int)ctx->Malloc;
     p.Z = (int)cfg.units;
     p.Zq = (int)Z;
@@ -1611,6 +1632,7 @@ sdtw_status sdtw_set_option(int key, int64_t v) {
         case SDTW_OPT_PRECISION: if (v != 8 && v != 16 && v != 32) break; g_opt.precision = (int)v; return SDTW_OK;
         case SDTW_OPT_Q8_PRUNE: if (v < -1 || v > 255) break; g_opt.q8_prune = (int)v; return SDTW_OK;
         case SDTW_OPT_Q8_CLIP: if (v < 0 || v >= 500000) break; g_opt.q8_clip = (int)v; return SDTW_OK;
+        case SDTW_OPT_QUERY_ROWS: if (v < 0 || v > 2) break; g_opt.query_rows = (int)v; return SDTW_OK;
         case SDTW_OPT_PAD: if (v < 0 || v > (1 << 20)) break; g_opt.pad = (int)v; return SDTW_OK;
         case SDTW_OPT_SPEC_ROUNDS: if (v < 0 || v > 4096) break; g_opt.spec_rounds = (int)v; return SDTW_OK;
         case SDTW_OPT_START: if (v < 0 || v > 2) break; g_opt.start = (int)v; return SDTW_OK;
@@ -1639,6 +1661,7 @@ sdtw_status sdtw_get_option(int key, int64_t* v) {
         case SDTW_OPT_PRECISION: *v = g_opt.precision; return SDTW_OK;
         case SDTW_OPT_Q8_PRUNE: *v = g_opt.q8_prune; return SDTW_OK;
         case SDTW_OPT_Q8_CLIP: *v = g_opt.q8_clip; return SDTW_OK;
+        case SDTW_OPT_QUERY_ROWS: *v = g_opt.query_rows; return SDTW_OK;
         case SDTW_OPT_STAT_FIXUP_DEPTH: {
             Ctx* ctx;
             const sdtw_status s = get_ctx(&ctx);
@@ -1705,6 +1728,7 @@ void sdtw_release(void) {
     cudaFree(c.ref_q8);
     cudaFree(c.q8_ws);
     cudaFree(c.ws_xq);
+    cudaFree(c.ws_xg);
     cudaFree(c.flag_d);
     cudaFreeHost(c.flag_h);
     cudaEventDestroy(c.ev0);

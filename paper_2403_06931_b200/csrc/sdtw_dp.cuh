@@ -121,7 +121,8 @@ struct DpParams {
     float* ckpt;
     float* ckpt_c;
     int ck_sg, ck_rc;
-    int q8_tau2;           // uint8-codebook kernels with INF pruning: tau^2 (sdtw_q8.cuh)
+    int q8_tau2;
+    const float* xg;       // XG kernels: query rows in the two-chain pair layout, q * PdMax * 2 floats per query           // uint8-codebook kernels with INF pruning: tau^2 (sdtw_q8.cuh)
 };
 
 template <bool TRACE> struct Entry { float d; };
@@ -419,7 +420,9 @@ struct SmemLayout {
 };
 // xs: "single" row layout (x_r alone, plain row order; C == 2 only): half the bytes per
 // row for long queries whose rows would otherwise cost a resident CTA, one more LDS per step.
-__host__ __device__ inline SmemLayout smem_layout(int C, int WC, bool trace, int GW, int Pd, int RS, bool xs = false) {
+// xg: the query rows live in a global pair-layout buffer (DpParams::xg), none in shared memory
+__host__ __device__ inline SmemLayout smem_layout(int C, int WC, bool trace, int GW, int Pd, int RS, bool xs = false,
+                                                  bool xg = false) {
     SmemLayout L;
     const int ent = trace ? 8 : 4;
     int o = 0;
@@ -427,7 +430,7 @@ __host__ __device__ inline SmemLayout smem_layout(int C, int WC, bool trace, int
     L.off_red = o;  o += 16 * (32 + 16);                // per-warp + per-rank partials
     L.off_inf = o;  o += 32 * 8;                        // +inf inbox entries (round 0)
     o = (o + 15) & ~15;
-    L.off_x = o;    o += xs ? Pd * 4 : xrow_stride(Pd, xrow_classes(C)) * xrow_classes(C) * xrow_floats(C) * 4;
+    L.off_x = o;    o += xg ? 0 : (xs ? Pd * 4 : xrow_stride(Pd, xrow_classes(C)) * xrow_classes(C) * xrow_floats(C) * 4);
     o = (o + 15) & ~15;
     L.off_bnd = o;  o += Pd * ent;
     o = (o + 15) & ~15;
@@ -752,9 +755,12 @@ __device__ __forceinline__ int fmod_pos(int a, int m) { int r = a % m; return r 
 __device__ __forceinline__ bool hits_row(int blo, int len, int row, int Pd) { return fmod_pos(row - blo, Pd) < len; }
 
 // ============================================================================ kernel
-template <int C, int WC, bool FMA, bool TRACE, bool CLUSTER, bool XS = false, bool CKPT = false>
+// XG: query rows read from the global pair-layout buffer P.xg (written by xg_layout_kernel) instead
+// of shared memory -- long queries, whose rows would otherwise cost a resident CTA
+template <int C, int WC, bool FMA, bool TRACE, bool CLUSTER, bool XS = false, bool CKPT = false, bool XG = false>
 __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2) sdtw_dp_kernel(const DpParams P) {
     static_assert(!XS || C == 2, "single-row layout is for two chains");
+    static_assert(!XG || (C == 2 && !XS && !TRACE && !CLUSTER), "global query rows: two-chain cost/end kernels");
     static_assert(!CKPT || (!TRACE && !CLUSTER && SDTW_FAST_RUNS), "round checkpoints: cost/end kernels without clusters");
     static_assert(C == 1 || C == 2 || C == 4, "chains per lane");
     static_assert(((WC + 1) & WC) == 0 && (32 * C) % (WC + 1) == 0 && (WC + 1) % C == 0,
@@ -776,11 +782,11 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     const int V = 32 * C * G;
     const int PdMax = P.Pd, K = P.K, RS = P.RS;
     const float nz = P.negzero;
-    const SmemLayout L = smem_layout(C, WC, TRACE, GW, PdMax, RS, XS);
+    const SmemLayout L = smem_layout(C, WC, TRACE, GW, PdMax, RS, XS, XG);
 
     int* pp = reinterpret_cast<int*>(smem + L.off_ctr);        // producer progress seen by warp w
     int* cp = pp + 32;                                          // consumer progress of w's successor
-    float* xs = reinterpret_cast<float*>(smem + L.off_x);
+    float* xs_sm = reinterpret_cast<float*>(smem + L.off_x);
     E* bnd = reinterpret_cast<E*>(smem + L.off_bnd);
     E* ring = reinterpret_cast<E*>(smem + L.off_ring);
     Partial* red = reinterpret_cast<Partial*>(smem + L.off_red);
@@ -869,6 +875,8 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     }
     const int Pl = pb - pa;                                 // rounds in this unit
     const int Mtot_bands = Pl * Pd;
+    // query rows of this unit: shared memory (filled by the prologue) or the global pair layout
+    const float* xs = XG ? P.xg + (long)q * PdMax * 2 : xs_sm;
     // round checkpoints of this unit: local round l -> ckb + l*Pd (rows [0, Pd))
     float* ckb = nullptr;
     if constexpr (CKPT) {
@@ -888,12 +896,14 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     // caller-supplied boundary column (sdtw_boundary_dp starts at round 0 from one)
     const bool lead_inf = pa == 0 && !(BDP && in_k == -2);
     for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
-        float* dst = XS ? xs + r : xs + (long)xrow_index(r, Pd, NC) * XC;
+        if constexpr (!XG) {
+            float* dst = XS ? xs_sm + r : xs_sm + (long)xrow_index(r, Pd, NC) * XC;
 #pragma unroll
-        for (int j = 0; j < XC; ++j) {
-            int rr = r - j;
-            if (rr < 0) rr += Pd;
-            dst[j] = (rr < N) ? xq[rr] : 0.0f;
+            for (int j = 0; j < XC; ++j) {
+                int rr = r - j;
+                if (rr < 0) rr += Pd;
+                dst[j] = (rr < N) ? xq[rr] : 0.0f;
+            }
         }
         E e;
         if (bnd_in) {
@@ -1315,6 +1325,29 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
 
 // Persistent scheduling epilogue: per query, the lexicographic (cost, col) minimum
 // over its segments' candidates (and that candidate's start column).
+// XG kernels: the query rows of every query in the shared-memory pair layout of the two-chain
+// kernel (row r -> word xrow_index(r, Pd, 2) = (x_r, x_{r-1}), rows >= N zero), in global
+// memory, PdMax * 2 floats per query; Pd per query = max(N_q, need) for ragged batches.
+static __global__ void __launch_bounds__(256) xg_layout_kernel(const float* __restrict__ X, int N, int PdMax, int need,
+                                                               const int64_t* __restrict__ qoff,
+                                                               const int* __restrict__ qlen, float* xg) {
+    const int q = blockIdx.x;
+    int n = N, Pd = PdMax;
+    const float* xq = X + (long)q * N;
+    if (qlen) {
+        n = qlen[q];
+        Pd = max(n, need);
+        xq = X + qoff[q];
+    }
+    float* base = xg + (long)q * PdMax * 2;
+    for (int r = threadIdx.x; r < Pd; r += blockDim.x) {
+        float* dst = base + (long)xrow_index(r, Pd, 2) * 2;
+        const int r1 = r >= 1 ? r - 1 : r - 1 + Pd;
+        dst[0] = r < n ? xq[r] : 0.0f;
+        dst[1] = r1 < n ? xq[r1] : 0.0f;
+    }
+}
+
 static __global__ void finalize_kernel(const Partial* __restrict__ cand, int Z, int S, const int* err_flag, float* out_cost,
                                 int64_t* out_end, int64_t* out_start) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;

@@ -21,4 +21,10 @@ DpKernel pick_dp_c2xs(int WC, bool fma) {
     if (WC != 15) return nullptr;
     return fma ? sdtw_dp_kernel<2, 15, true, false, false, true> : sdtw_dp_kernel<2, 15, false, false, false, true>;
 }
+// query rows in global memory (XG: long queries, see smem_layout): cost/end, no cluster
+DpKernel pick_dp_c2xg(int WC, bool fma) {
+    if (WC != 15) return nullptr;
+    return fma ? sdtw_dp_kernel<2, 15, true, false, false, false, false, true>
+               : sdtw_dp_kernel<2, 15, false, false, false, false, false, true>;
+}
 }  // namespace sdtw

@@ -15,7 +15,8 @@ DpKernel pick_dpq_c2(int WC, bool fma, bool trace);
 DpKernel pick_dp16(int WC);
 DpKernel pick_dp8(int WC, bool prune);      // uint8 codebook (sdtw_dp8.cu)
 DpKernel pick_dp_c2xs(int WC, bool fma);
-DpKernel pick_dp_c2ck(int WC, bool fma, bool xs);   // + round checkpoints (sdtw_dp_c2k.cu)
+DpKernel pick_dp_c2xg(int WC, bool fma);            // query rows in global memory
+DpKernel pick_dp_c2ck(int WC, bool fma, int xs);    // + round checkpoints (sdtw_dp_c2k.cu)
 inline DpKernel pick_dp(int C, int WC, bool fma, bool trace, bool cl) {
     switch (C) {
         case 1: return trace ? pick_dp_c1t(WC, fma, cl) : pick_dp_c1(WC, fma, cl);

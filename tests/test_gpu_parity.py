@@ -324,3 +324,22 @@ def test_max_size_reference_exact_match_at_the_far_end():
     sd.release()
     rc = sd._lib.sdtw_set_reference(ctypes.c_void_p(Q.ctypes.data), ctypes.c_int64(0x7fffffff))
     assert rc == sd.E_ARG
+
+
+@pytest.mark.parametrize("fma", [1, 0])
+@pytest.mark.parametrize("Z,N,M,opts", [
+    (8, 64, 4096, dict()), (5, 300, 20001, dict()), (3, 1, 500, dict()), (4, 257, 3001, dict(OPT_LANES=2)),
+    (6, 1000, 100_000, dict(OPT_SCHED=2, OPT_SEGMENTS=3)), (6, 1000, 100_000, dict(OPT_SCHED=3)),
+    (6, 700, 50_000, dict(OPT_SCHED=1)),
+])
+def test_query_rows_in_global_memory(fma, Z, N, M, opts):
+    """SDTW_OPT_QUERY_ROWS=2 (XG kernels: the query rows in a global pair-layout buffer instead
+    of shared memory, the auto choice for long queries): bit-exact against the oracle for
+    cost/end and the checkpointed start index, across schedules."""
+    Q, Y = _inputs(Z, N, M, 90 + N)
+    ref = oracle.sdtw(Q, Y, fma=bool(fma), start=True, last_rows=True)
+    got = _gpu(Q, Y, OPT_FMA=fma, OPT_QUERY_ROWS=2, **opts)
+    _check_exact(Q, Y, got, fma=bool(fma), ref=ref)
+    if opts.get("OPT_SCHED") != 1:
+        got_t = _gpu(Q, Y, trace=True, OPT_FMA=fma, OPT_QUERY_ROWS=2, OPT_START=2, **opts)
+        _check_exact(Q, Y, got_t, fma=bool(fma), trace=True, ref=ref)
