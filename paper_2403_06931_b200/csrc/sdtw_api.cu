@@ -15,6 +15,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -319,6 +320,9 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     }
     *cfg = LaunchCfg{C, WC, GW, CL, K, RS, (int)Pd, (int)Pr, L.bytes, 0, 1, 0, dual ? 1 : 0, units, (int)need,
                      half, xs};
+    if (getenv("SDTW_DEBUG_PLAN"))                      // diagnostics only
+        fprintf(stderr, "[sdtw plan] Z=%lld N=%lld C=%d WC=%d GW=%d K=%d RS=%d Pd=%lld Pr=%lld smem=%d rows=%d\n",
+                (long long)Z, (long long)N, C, WC, GW, K, RS, (long long)Pd, (long long)Pr, L.bytes, xs);
     // Persistent scheduling (default when a cluster is not requested): k resident CTAs
     // per SM, k = min(occupancy, rings / SMs), pull (ring, round-segment) units, so every
     // SM carries the same load whatever the batch size mod #SMs is.
