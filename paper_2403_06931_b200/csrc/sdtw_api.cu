@@ -14,6 +14,7 @@
 #include "sdtw_start.cuh"
 
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1089,11 +1090,18 @@ sdtw_status run_traceback_ckpt(const float* Q, int64_t Z, int64_t N, float* out_
         return fail(SDTW_E_ARG, "checkpointed start index needs the two-chain fp32 cost/end kernel");
     const size_t per = (size_t)cfg.Pr * cfg.Pd;
     const size_t ck_bytes = (size_t)Z * per * sizeof(float);
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); free_b = 0; }
+    const bool dbg = getenv("SDTW_DEBUG_PLAN") != nullptr;
+    auto now_ms = []() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t_a = dbg ? now_ms() : 0.0;
+    // (cudaMemGetInfo only when the checkpoints must grow: it stalled 8-40 ms now and then,
+    // r02 probe at config 5)
     const size_t have_b = ctx->ws_ck_n * sizeof(float);
-    if (ck_bytes > have_b && ck_bytes > (free_b + have_b) / 2)
-        return fail(SDTW_E_ARG, "round checkpoints exceed half the free device memory");
+    if (ck_bytes > have_b) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); free_b = 0; }
+        if (ck_bytes > (free_b + have_b) / 2)
+            return fail(SDTW_E_ARG, "round checkpoints exceed half the free device memory");
+    }
     s = grow(&ctx->ws_ck, &ctx->ws_ck_n, (size_t)Z * per);
     if (s != SDTW_OK) return s;
     const int64_t launches0 = g_launches.load();
@@ -1107,7 +1115,9 @@ sdtw_status run_traceback_ckpt(const float* Q, int64_t Z, int64_t N, float* out_
     const Options o = g_opt;
     cudaStream_t st = o.stream;
     float ms_dp = 0.0f;
+    const double t_b = dbg ? now_ms() : 0.0;
     s = run_batch(Q, Z, N, out_cost, out_end, nullptr, false, &bd, Ragged(), &r);
+    const double t_c = dbg ? now_ms() : 0.0;
     if (s != SDTW_OK) return s;
     ms_dp = (float)ctx->last_dp_ms;
     const int ks = ptr_kind(out_start);
@@ -1202,8 +1212,9 @@ sdtw_status run_traceback_ckpt(const float* Q, int64_t Z, int64_t N, float* out_
             wp.path_hi = dhi;
             wp.err_flag = ctx->flag_d;
             const int T = (int)std::min<int64_t>(256, (N + 31) / 32 * 32);
-            if (o.fma) sdtw::window_dp_kernel<true><<<(unsigned)n, T, 2 * T * sizeof(float), st>>>(wp);
-            else sdtw::window_dp_kernel<false><<<(unsigned)n, T, 2 * T * sizeof(float), st>>>(wp);
+            const size_t wsm = 2 * (size_t)T * sdtw::kWinStrip * sizeof(float);
+            if (o.fma) sdtw::window_dp_kernel<true><<<(unsigned)n, T, wsm, st>>>(wp);
+            else sdtw::window_dp_kernel<false><<<(unsigned)n, T, wsm, st>>>(wp);
             sdtw::window_walk_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(wp, (int)n);
             CK(cudaGetLastError());
             g_launches += 2;
@@ -1240,6 +1251,9 @@ sdtw_status run_traceback_ckpt(const float* Q, int64_t Z, int64_t N, float* out_
     CK(cudaStreamSynchronize(st));
     ctx->last_launches = g_launches.load() - launches0;
     ctx->last_start_iters = iters;
+    if (dbg)
+        fprintf(stderr, "[sdtw start] setup %.2f ms, cost/end+checkpoints %.2f ms, windows %.2f ms (%d iterations)\n",
+                t_b - t_a, t_c - t_b, now_ms() - t_c, iters);
     return SDTW_OK;
 }
 

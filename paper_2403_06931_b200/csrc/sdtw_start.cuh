@@ -74,12 +74,18 @@ __device__ __forceinline__ float win_cell(float x, float y, float m) {
     return __fadd_rn(__fmul_rn(t, t), m);
 }
 
-// One CTA per window: T threads own T consecutive query rows (a band) and sweep the
-// window's anti-diagonals with one barrier per step (the path_dp_kernel scheme, from a
-// checkpoint boundary instead of +inf).
+// One CTA per window: T threads own T consecutive query rows (a band) and sweep the window
+// in strips of WS columns: at step s thread k computes its row's columns [WS(s-k), WS(s-k)+WS)
+// -- a strip whose up inputs thread k-1 produced at step s-1 (shared memory) -- so one
+// barrier covers WS cells per thread (the path_dp_kernel scheme with WS = 1 needed one barrier
+// and ~60 instructions per cell; ncu r02, config 5 N = 8,000).  Every cell is the DP kernel's
+// cell from the checkpoint boundary (exact), and records its argmin predecessor as a 2-bit
+// code (0 diag, 1 up, 2 left, priority in that order), 16 codes per word.
+constexpr int kWinStrip = 8;
 template <bool FMA>
 __global__ void __launch_bounds__(256) window_dp_kernel(const WinParams P) {
-    extern __shared__ float pvals[];                 // [2][T]
+    constexpr int WS = kWinStrip;
+    extern __shared__ __align__(16) float pvals[];   // [2][T][WS]: the strips of the last two steps
     const int z = blockIdx.x;
     const int q = P.qidx[z];
     const int T = blockDim.x, k = threadIdx.x;
@@ -87,6 +93,7 @@ __global__ void __launch_bounds__(256) window_dp_kernel(const WinParams P) {
     if (!(c < INFINITY)) return;
     const int64_t j0 = (int64_t)P.k0[z] * P.cpr;
     const int L = (int)(P.end[q] - j0 + 1);
+    const int nst = (L + WS - 1) / WS;               // strips in the window
     const int N = P.N;
     const float* xq = P.X + (int64_t)q * N;
     const float* yw = P.Y + j0;
@@ -95,40 +102,91 @@ __global__ void __launch_bounds__(256) window_dp_kernel(const WinParams P) {
     float* rb = P.rowbuf + (int64_t)z * P.Lmax;
     const float INF = INFINITY;
 
-    for (int band = 0; band * T < N; ++band) {
-        const int i = band * T + k;
-        const bool live = i < N;
-        const float x = live ? xq[i] : 0.0f;
-        // column j0 - 1: the checkpoint (exact) or +inf; row -1: the free start (0)
-        float up_prev = (i == 0) ? 0.0f : (bnd && live ? bnd[i - 1] : INF);   // D(i-1, j0-1)
-        float left = (bnd && live) ? bnd[i] : INF;                              // D(i, j0-1)
-        uint32_t word = 0;
-        const int steps = L + T - 1;
-        for (int s = 0; s < steps; ++s) {
-            const int j = s - k;
-            float v = INF;
-            if (live && j >= 0 && j < L) {
-                float up;
-                if (k == 0) up = (band == 0) ? 0.0f : rb[j];
-                else up = pvals[((s - 1) & 1) * T + k - 1];
-                const float diag = up_prev;
-                const float m = fminf(fminf(diag, up), left);
-                v = win_cell<FMA>(x, yw[j], m);
-                const uint32_t code = (diag == m) ? 0u : ((up == m) ? 1u : 2u);
-                word |= code << (2 * (j & 15));
-                if ((j & 15) == 15 || j == L - 1) {
-                    cq[(int64_t)i * P.W + (j >> 4)] = word;
-                    word = 0;
-                }
-                up_prev = up;
-                left = v;
-                if (i == N - 1 && j == L - 1 && v != c) atomicExch(P.err_flag, 2);
+    // Rows wrap around the T threads: thread k owns rows k, k+T, k+2T, ... and spends P =
+    // max(nst, T) steps per row (nst of them computing), so row k+T*r, strip js runs at step
+    // k + r*P + js: its up strip (row - 1) was computed one step earlier by thread k-1 (shared
+    // memory), or -- thread 0 -- at least one step earlier by thread T-1 of the previous cycle
+    // (rb).  The threads stay busy across rows instead of draining after each band of T rows.
+    const int Pp = max(nst, T);
+    const int cycles = (N + T - 1) / T;
+    const int steps = (T - 1) + cycles * Pp;
+    int r = 0, js = -k;                              // this thread's cycle and strip at step s
+    float up_prev = 0.0f, left = INF, x = 0.0f;
+    uint32_t word = 0;
+    for (int s = 0; s < steps; ++s) {
+        const int i = r * T + k;
+        float v[WS];
+#pragma unroll
+        for (int e = 0; e < WS; ++e) v[e] = INF;
+        if (i < N && js >= 0 && js < nst) {
+            if (js == 0) {                           // a new row: its sample and left boundary
+                x = xq[i];
+                // column j0 - 1: the checkpoint (exact) or +inf; row -1: the free start (0)
+                up_prev = (i == 0) ? 0.0f : (bnd ? bnd[i - 1] : INF);   // D(i-1, j0-1)
+                left = bnd ? bnd[i] : INF;                              // D(i, j0-1)
+                word = 0;
             }
-            pvals[(s & 1) * T + k] = v;
-            if (k == T - 1 && live && j >= 0 && j < L) rb[j] = v;
-            __syncthreads();
+            const int jb = js * WS;
+            float up[WS];
+            if (k == 0) {
+#pragma unroll
+                for (int e = 0; e < WS; ++e) up[e] = (i == 0) ? 0.0f : (jb + e < L ? rb[jb + e] : INF);
+            } else {
+                const float4* pv = reinterpret_cast<const float4*>(pvals + (((s - 1) & 1) * T + k - 1) * WS);
+#pragma unroll
+                for (int e = 0; e < WS / 4; ++e) {
+                    const float4 t4 = pv[e];
+                    up[4 * e] = t4.x; up[4 * e + 1] = t4.y; up[4 * e + 2] = t4.z; up[4 * e + 3] = t4.w;
+                }
+            }
+            const bool full = jb + WS <= L;          // every strip but possibly the last
+            float yv[WS];
+            if (full) {                              // yw is 16-byte aligned (j0 is a round start)
+                const float4* y4 = reinterpret_cast<const float4*>(yw + jb);
+#pragma unroll
+                for (int e = 0; e < WS / 4; ++e) {
+                    const float4 t4 = __ldg(y4 + e);
+                    yv[4 * e] = t4.x; yv[4 * e + 1] = t4.y; yv[4 * e + 2] = t4.z; yv[4 * e + 3] = t4.w;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < WS; ++e) yv[e] = jb + e < L ? yw[jb + e] : 0.0f;
+            }
+            uint32_t half = 0;                       // this strip's WS codes (2 bits each)
+#pragma unroll
+            for (int e = 0; e < WS; ++e) {
+                if (full || jb + e < L) {
+                    const float diag = (e == 0) ? up_prev : up[e - 1];
+                    const float m = fminf(fminf(diag, up[e]), left);
+                    v[e] = win_cell<FMA>(x, yv[e], m);
+                    const uint32_t code = (diag == m) ? 0u : ((up[e] == m) ? 1u : 2u);
+                    half |= code << (2 * e);
+                    left = v[e];
+                }
+            }
+            // 16 codes per word = two strips: the even strip starts the word, the odd one
+            // completes and stores it (or the last strip stores what it has)
+            static_assert(WS == 8, "two strips per 16-code word");
+            if ((js & 1) == 0) word = half;
+            else word |= half << 16;
+            if ((js & 1) == 1 || js == nst - 1) cq[(int64_t)i * P.W + (jb >> 4)] = word;
+            if (i == N - 1 && js == nst - 1) {      // the window reproduces the batch cost
+#pragma unroll
+                for (int e = 0; e < WS; ++e)
+                    if (jb + e == L - 1 && v[e] != c) atomicExch(P.err_flag, 2);
+            }
+            up_prev = up[WS - 1];
+            if (k == T - 1) {                        // the next cycle's thread 0 reads this row
+#pragma unroll
+                for (int e = 0; e < WS; ++e)
+                    if (jb + e < L) rb[jb + e] = v[e];
+            }
         }
+        float* pw = pvals + ((s & 1) * T + k) * WS;
+#pragma unroll
+        for (int e = 0; e < WS; ++e) pw[e] = v[e];
         __syncthreads();
+        if (++js == Pp) { js = 0; ++r; }
     }
 }
 
