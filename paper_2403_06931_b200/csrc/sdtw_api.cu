@@ -86,7 +86,10 @@ struct Ctx {
     double last_win_ms = 0.0;                       // checkpointed start index: window phase time
     int last_start_iters = 0;                       // ... and its window-widening iterations
     int64_t last_fixups = 0;                        // queries recomputed by the last call
-    int64_t order_key[3] = {-1, -1, -1};
+    // grab order / unit table of the last persistent launch, reused while the plan is the
+    // same (a per-call host simulation + synchronous copies left the GPU idle ~0.1-0.5 ms)
+    int64_t order_key[7] = {-1, -1, -1, -1, -1, -1, -1};
+    int64_t utab_key[3] = {-1, -1, -1};
     // uint8 codebook (NEXT-3, sdtw_q8.cuh): codes of the reference as fp32 0..255 (Malloc,
     // padded 0), the codebook {lo, hi} on the device and host, radix-select workspace
     float* ref_q8 = nullptr;
@@ -897,6 +900,8 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.bnd_user = nullptr;
     p.col_out = nullptr;
     p.negzero = -0.0f;
+    // plain cost/end calls consume no end column of the last round (tail skip)
+    p.tail_skip = (smode == 0 && !cfg.ck && getenv("SDTW_NO_TAIL_SKIP") == nullptr) ? 1 : 0;
     p.ckpt = nullptr;
     p.ckpt_c = nullptr;
     p.ck_sg = 0;
@@ -931,10 +936,15 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
         p.cand = b + 256 + done_b + fix_b;
         p.bnd_g = static_cast<unsigned char*>(p.cand) + 16 * (size_t)Z * cfg.S;
         CK(cudaMemsetAsync(b, 0, 256 + done_b, st));
-        if (cfg.spec) {
+        const bool utab_hit = cfg.spec && smode != 2 && ctx->utab_key[0] == cfg.Pr &&
+                              ctx->utab_key[1] == cfg.Sseg && ctx->utab_key[2] == cfg.Rc;
+        if (cfg.spec && utab_hit) {
+            p.utab = ctx->utab_d;
+        } else if (cfg.spec) {
             const std::vector<int4> tab = smode == 2
                 ? std::vector<int4>{make_int4(0, cfg.Rc, sr->bnd ? -2 : -1, sr->free_start ? 0 : 1)}
                 : spec_table(cfg.Pr, cfg.Sseg, cfg.Rc);
+            ctx->utab_key[0] = -1;
             if (tab.size() > ctx->utab_n) {
                 if (ctx->utab_d) cudaFree(ctx->utab_d);
                 ctx->utab_d = nullptr;
@@ -944,9 +954,17 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
             }
             CK(cudaMemcpy(ctx->utab_d, tab.data(), tab.size() * sizeof(int4), cudaMemcpyHostToDevice));
             p.utab = ctx->utab_d;
+            if (smode != 2) {
+                ctx->utab_key[0] = cfg.Pr;
+                ctx->utab_key[1] = cfg.Sseg;
+                ctx->utab_key[2] = cfg.Rc;
+            }
         }
-        if (cfg.spec || rg.off || ctx->order_key[0] != (int64_t)R || ctx->order_key[1] != cfg.S ||
-            ctx->order_key[2] != cfg.workers) {
+        const int64_t okey[7] = {(int64_t)R, cfg.S, cfg.workers, cfg.spec, cfg.spec ? cfg.Pr : 0,
+                                 cfg.spec ? cfg.Sseg : 0, cfg.spec ? cfg.Rc : 0};
+        bool order_hit = !rg.off && smode != 2;
+        for (int k = 0; k < 7; ++k) order_hit = order_hit && ctx->order_key[k] == okey[k];
+        if (!order_hit) {
             std::vector<int> ord;
             if (smode == 2) {
                 ord.resize(R);
@@ -975,9 +993,8 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
                 ctx->order_n = ord.size();
             }
             CK(cudaMemcpy(ctx->order_d, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice));
-            ctx->order_key[0] = (rg.off || cfg.spec) ? -1 : (int64_t)R;   // ragged / speculative: not cached
-            ctx->order_key[1] = cfg.S;
-            ctx->order_key[2] = cfg.workers;
+            for (int k = 0; k < 7; ++k) ctx->order_key[k] = okey[k];
+            if (rg.off || smode == 2) ctx->order_key[0] = -1;       // ragged / boundary DP: not cached
         }
         p.order = ctx->order_d;
     }

@@ -122,6 +122,7 @@ struct DpParams {
     float* ckpt_c;
     int ck_sg, ck_rc;
     int q8_tau2;
+    int tail_skip;         // 1: warps stop one round early where the unit's last round is beyond M (no end column consumed)
     const float* xg;       // XG kernels: query rows in the two-chain pair layout, q * PdMax * 2 floats per query           // uint8-codebook kernels with INF pruning: tau^2 (sdtw_q8.cuh)
 };
 
@@ -955,14 +956,26 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     int p0 = (b0 < 0) ? -1 : 0;
     int r0 = (b0 < 0) ? b0 + Pd : 0;
 
-    // warp g runs steps [32*C*g, 32*C*g + span): its lanes' bands cover [0, Pr*Pd)
-    const int span = (32 * C - 1 + Mtot_bands + K - 1) / K * K;
+    // warp g runs steps [32*C*g, 32*C*g + span_g): its lanes' bands cover [0, Pl*Pd).
+    // Tail skip (P.tail_skip, calls that consume no end column): in the unit's last round a
+    // warp whose strips all lie beyond the reference (the partial last round of the whole
+    // reference: config 2 has 26.04 rounds) would compute only +inf cells, so its bands
+    // stop one round early and its SMSP issue goes to the other resident rings.  Monotone
+    // in g: the skipping warps are a suffix of the ring.
+    auto bands_of = [&](int g) -> int {
+        if (!CKPT && P.tail_skip && Pl > 1 && ((long)(pa + Pl - 1) * V + 32L * C * g) * WC >= (long)P.M)
+            return Mtot_bands - Pd;
+        return Mtot_bands;
+    };
+    auto span_of = [&](int g) { return (32 * C - 1 + bands_of(g) + K - 1) / K * K; };
+    const bool tail_skipped = bands_of(gw) < Mtot_bands;
+    const int span = span_of(gw);
     const int t_begin = u_min;
     const int t_end = t_begin + span;
     // a predecessor never publishes past its own end: the successor's trailing
     // (idle-band) chunks must not wait for more
-    const int pred_end = t_end - 32 * C;                 // = t_end of warp gw-1
-    const int last_end = 32 * C * (G - 1) + span;        // = t_end of warp G-1
+    const int pred_end = gw > 0 ? u_min - 32 * C + span_of(gw - 1) : 0;   // = t_end of warp gw-1
+    const int last_end = 32 * C * (G - 1) + span_of(G - 1);              // = t_end of warp G-1
     const unsigned FULL = 0xffffffffu;
 
     // Reference strips for the lanes' round transitions are staged in shared memory
@@ -1260,6 +1273,9 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         if (lane == 31) st_release_hop(succ_pp, t0 + K, succ_remote);
         if (lane == 0 && gw > 0) st_release_hop(pred_cp, t0 + K, pred_remote);
     }
+    // a tail-skipping warp consumes nothing more: its (non-skipping) predecessor must never
+    // wait for ring space again (reset by the next unit's prologue)
+    if (tail_skipped && lane == 0 && gw > 0) st_release_hop(pred_cp, INT_MAX / 2, pred_remote);
 
     // ---- reduction of (cost, col[, start]) over chains, lanes, warps, cluster CTAs
     float bc = best[0];
