@@ -680,7 +680,11 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
 std::vector<int4> spec_table(int Pr, int Sg, int Rc) {
     std::vector<int4> t(3 * Sg - 1);
     for (int s = 0; s < Sg; ++s) {
-        const int a = (int)((int64_t)s * Pr / Sg), e = (int)((int64_t)(s + 1) * Pr / Sg);
+        int a = (int)((int64_t)s * Pr / Sg), e = (int)((int64_t)(s + 1) * Pr / Sg);
+        if (const char* sp = getenv("SDTW_SPEC_SPLIT")) {       // (experiment, cost/end, Sg = 2)
+            const int b = atoi(sp);
+            if (Sg == 2 && b > Rc && b < Pr - Rc) { a = s == 0 ? 0 : b; e = s == 0 ? b : Pr; }
+        }
         t[s] = make_int4(a, a + Rc, -1, 0);
         t[Sg + s] = make_int4(a + Rc, e, s, 0);
         if (s > 0) t[2 * Sg + s - 1] = make_int4(a, a + Rc, Sg + s - 1, 1);
@@ -901,6 +905,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     p.col_out = nullptr;
     p.negzero = -0.0f;
     // plain cost/end calls consume no end column of the last round (tail skip)
+    p.unit_log = nullptr;
     p.tail_skip = (smode == 0 && !cfg.ck && getenv("SDTW_NO_TAIL_SKIP") == nullptr) ? 1 : 0;
     p.ckpt = nullptr;
     p.ckpt_c = nullptr;
@@ -1000,9 +1005,33 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     }
     p.bnd_user = smode == 2 ? sr->bnd : nullptr;
     p.col_out = smode == 2 ? sr->col_out : nullptr;
+    // diagnostics: SDTW_UNIT_LOG=<file> appends one line per grabbed unit of this launch
+    // (unit, SM, block, grab / start / end ns) -- scripts/unit_timeline.py reads it
+    const char* ulog_path = cfg.persistent ? getenv("SDTW_UNIT_LOG") : nullptr;
+    long long* ulog_d = nullptr;
+    const size_t ulog_n = ulog_path ? (size_t)cfg.units * cfg.S : 0;
+    if (ulog_path) {
+        CK(cudaMalloc(&ulog_d, ulog_n * 4 * sizeof(long long)));
+        CK(cudaMemsetAsync(ulog_d, 0, ulog_n * 4 * sizeof(long long), st));
+        p.unit_log = ulog_d;
+    }
     if (o.profile) CK(cudaEventRecord(ctx->ev0, st));
     s = launch_dp(cfg, o.fma != 0, trace, p, st);
     if (s != SDTW_OK) return s;
+    if (ulog_path) {
+        std::vector<long long> h(ulog_n * 4);
+        CK(cudaStreamSynchronize(st));
+        CK(cudaMemcpy(h.data(), ulog_d, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        cudaFree(ulog_d);
+        if (FILE* f = fopen(ulog_path, "a")) {
+            fprintf(f, "# launch Z=%lld S=%d Sseg=%d Rc=%d Pr=%d workers=%d\n", (long long)cfg.units, cfg.S, cfg.Sseg,
+                    cfg.Rc, cfg.Pr, cfg.workers);
+            for (size_t i = 0; i < ulog_n; ++i)
+                fprintf(f, "%zu %lld %lld %lld %lld %lld %lld\n", i, h[4 * i] & 0xfffff, (h[4 * i] >> 20) & 0xfffff,
+                        h[4 * i] >> 40, h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+            fclose(f);
+        }
+    }
     if (smode == 2) {
         sdtw::finalize_kernel<<<(unsigned)((Z + 127) / 128), 128, 0, st>>>(
             static_cast<const sdtw::Partial*>(p.cand), (int)Z, 1, ctx->flag_d, dc, de, nullptr);

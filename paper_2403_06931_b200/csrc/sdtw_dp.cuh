@@ -122,6 +122,7 @@ struct DpParams {
     float* ckpt_c;
     int ck_sg, ck_rc;
     int q8_tau2;
+    long long* unit_log;   // diagnostics (SDTW_UNIT_LOG): per grabbed unit {sm<<40|block<<20|unit, grab, start, end} ns
     int tail_skip;         // 1: warps stop one round early where the unit's last round is beyond M (no end column consumed)
     const float* xg;       // XG kernels: query rows in the two-chain pair layout, q * PdMax * 2 floats per query           // uint8-codebook kernels with INF pruning: tau^2 (sdtw_q8.cuh)
 };
@@ -130,6 +131,11 @@ template <bool TRACE> struct Entry { float d; };
 template <> struct Entry<true> { float d; int s; };
 
 // ------------------------------------------------------------ synchronisation
+__device__ __forceinline__ long long globaltimer_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void st_release_cluster(int* p, int v) {
     asm volatile("st.release.cluster.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -826,6 +832,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     constexpr int XC = XS ? 1 : xrow_floats(C);
     constexpr int NC = XS ? 1 : xrow_classes(C);
     int* unit_sh = pp + 64;                                     // broadcast of the grabbed unit
+    long long* log_slot = nullptr;                              // diagnostics (P.unit_log), thread 0
     for (int unit_iter = 0;; ++unit_iter) {
     // ---- which unit: (query q, rounds [pa, pb))
     int q, seg = 0, pa = 0, pb = P.Pr;
@@ -837,6 +844,13 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         if (threadIdx.x == 0) {
             const int raw = atomicAdd(P.counter, 1);
             *unit_sh = (P.order && raw < P.Z * P.S) ? P.order[raw] : raw;
+            log_slot = (P.unit_log && raw < P.Z * P.S) ? P.unit_log + 4L * raw : nullptr;
+            if (log_slot) {
+                unsigned sm;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+                log_slot[0] = ((long long)sm << 40) | ((long long)blockIdx.x << 20) | *unit_sh;
+                log_slot[1] = globaltimer_ns();
+            }
         }
         __syncthreads();
         const int u = *unit_sh;
@@ -861,6 +875,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                 if (++n == (1LL << 26)) { printf("sdtw watchdog: unit %d waits segment\n", u); __trap(); }
             }
         }
+        if (log_slot) log_slot[2] = globaltimer_ns();
         __syncthreads();
     } else {
         if (unit_iter > 0) break;
@@ -1332,6 +1347,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
             __threadfence();
             if (spec) st_release_gpu(P.seg_done + q * P.S + seg, 1);
             else st_release_gpu(P.seg_done + q, seg + 1);
+            if (log_slot) log_slot[3] = globaltimer_ns();
         }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
