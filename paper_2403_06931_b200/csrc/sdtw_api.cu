@@ -101,6 +101,7 @@ struct Ctx {
     int* flag_d = nullptr;
     int* flag_h = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_sched = nullptr;   // after the last launch that read order_d / utab_d
     double last_dp_ms = 0.0;
     int64_t last_launches = 0;
 };
@@ -135,6 +136,7 @@ sdtw_status get_ctx(Ctx** out) {
         CK(cudaMalloc(&c.ws_part, sizeof(double) * (4 * 4096 + 8)));   // 4 doubles per partial
         CK(cudaEventCreate(&c.ev0));
         CK(cudaEventCreate(&c.ev1));
+        CK(cudaEventCreateWithFlags(&c.ev_sched, cudaEventDisableTiming));
         c.init = true;
     }
     *out = &c;
@@ -957,7 +959,9 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
                 CK(cudaMalloc(&ctx->utab_d, tab.size() * sizeof(int4)));
                 ctx->utab_n = tab.size();
             }
-            CK(cudaMemcpy(ctx->utab_d, tab.data(), tab.size() * sizeof(int4), cudaMemcpyHostToDevice));
+            // the previous launch that read the table may still run (on this or another stream)
+            CK(cudaStreamWaitEvent(st, ctx->ev_sched, 0));
+            CK(cudaMemcpyAsync(ctx->utab_d, tab.data(), tab.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
             p.utab = ctx->utab_d;
             if (smode != 2) {
                 ctx->utab_key[0] = cfg.Pr;
@@ -997,7 +1001,8 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
                 CK(cudaMalloc(&ctx->order_d, ord.size() * sizeof(int)));
                 ctx->order_n = ord.size();
             }
-            CK(cudaMemcpy(ctx->order_d, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice));
+            CK(cudaStreamWaitEvent(st, ctx->ev_sched, 0));
+            CK(cudaMemcpyAsync(ctx->order_d, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice, st));
             for (int k = 0; k < 7; ++k) ctx->order_key[k] = okey[k];
             if (rg.off || smode == 2) ctx->order_key[0] = -1;       // ragged / boundary DP: not cached
         }
@@ -1018,6 +1023,7 @@ sdtw_status run_batch(const float* Q, int64_t Z, int64_t N, float* out_cost, int
     if (o.profile) CK(cudaEventRecord(ctx->ev0, st));
     s = launch_dp(cfg, o.fma != 0, trace, p, st);
     if (s != SDTW_OK) return s;
+    if (cfg.persistent) CK(cudaEventRecord(ctx->ev_sched, st));
     if (ulog_path) {
         std::vector<long long> h(ulog_n * 4);
         CK(cudaStreamSynchronize(st));
@@ -1796,6 +1802,7 @@ void sdtw_release(void) {
     cudaFree(c.flag_d);
     cudaFreeHost(c.flag_h);
     cudaEventDestroy(c.ev0);
+    cudaEventDestroy(c.ev_sched);
     cudaEventDestroy(c.ev1);
     c = Ctx();
 }
