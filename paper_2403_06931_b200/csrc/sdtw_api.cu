@@ -368,7 +368,9 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
         int64_t Sg = o.segments > 0 ? o.segments : (10 * W + units) / (2 * units);
         Sg = std::min<int64_t>(Sg, Pr / std::max<int64_t>(4 * (Rc + 1), 8));
         Sg = std::max<int64_t>(Sg, 2);
-        if (Pr / Sg <= Rc) return fail(SDTW_E_ARG, "speculative segments shorter than the correction pass");
+        for (int sg = 0; sg < (int)Sg; ++sg)
+            if (sdtw::spec_seg_start(sg + 1, (int)Pr, (int)Sg) - sdtw::spec_seg_start(sg, (int)Pr, (int)Sg) <= Rc)
+                return fail(SDTW_E_ARG, "speculative segments shorter than the correction pass");
         cfg->spec = 1;
         cfg->Sseg = (int)Sg;
         cfg->Rc = Rc;
@@ -676,17 +678,13 @@ sdtw_status spec_fixup(Ctx* ctx, const float* xd, int64_t Z, int64_t N, const st
 }
 
 // Speculative segments: the unit-kind table {pa, pb, in_k, db} of one
-// ring -- A_s (k = s): rounds [s*Pr/Sg, +Rc) from a +inf boundary; B_s (k = Sg + s): the
+// ring -- A_s (k = s): rounds [a_s, +Rc) from a +inf boundary (a_s = spec_seg_start); B_s (k = Sg + s): the
 // rest of segment s after A_s; C_s (k = 2Sg + s - 1, s >= 1): A_s's rounds again from
 // B_{s-1}'s end column with no free start.
 std::vector<int4> spec_table(int Pr, int Sg, int Rc) {
     std::vector<int4> t(3 * Sg - 1);
     for (int s = 0; s < Sg; ++s) {
-        int a = (int)((int64_t)s * Pr / Sg), e = (int)((int64_t)(s + 1) * Pr / Sg);
-        if (const char* sp = getenv("SDTW_SPEC_SPLIT")) {       // (experiment, cost/end, Sg = 2)
-            const int b = atoi(sp);
-            if (Sg == 2 && b > Rc && b < Pr - Rc) { a = s == 0 ? 0 : b; e = s == 0 ? b : Pr; }
-        }
+        const int a = sdtw::spec_seg_start(s, Pr, Sg), e = sdtw::spec_seg_start(s + 1, Pr, Sg);
         t[s] = make_int4(a, a + Rc, -1, 0);
         t[Sg + s] = make_int4(a + Rc, e, s, 0);
         if (s > 0) t[2 * Sg + s - 1] = make_int4(a, a + Rc, Sg + s - 1, 1);

@@ -33,13 +33,24 @@
 
 namespace sdtw {
 
+// First round a_s of speculative segment s of Sg (host plan spec_table() and this merge).
+// Equal segments, except the two-segment plan: there the first segment takes 16/25 of the
+// rounds.  Its chain A_0 -> B_0 -> C_1 carries the correction and should be the longer one;
+// measured at the config-2 shape (512 x 2,000, Pr = 25..30 rounds, profiles/r02al-r02am, r02ar)
+// the midpoint split ran at 6.7-7.4 TCUPS depending on Pr (equal B units leave a tail of
+// late long units) and a 0.64 split at 7.3-7.6 everywhere.
+__host__ __device__ inline int spec_seg_start(int s, int Pr, int Sg) {
+    if (Sg == 2 && s == 1) return (int)((int64_t)Pr * 16 / 25);
+    return (int)((int64_t)s * Pr / Sg);
+}
+
 // ck[q][a_s + j][r] = min(ck[q][a_s + j][r], ckc[q][s-1][j][r]) for s >= 1, j < Rc, r < N,
 // skipping queries marked for recomputation (fix[q] != 0).  grid (Sg-1, Z), block over rows.
 static __global__ void merge_ckpt_kernel(float* ck, const float* __restrict__ ckc, const int* __restrict__ fix,
                                          int Pr, int Pd, int N, int Sg, int Rc) {
     const int s = blockIdx.x + 1, q = blockIdx.y;
     if (fix && fix[q]) return;
-    const int a = (int)((int64_t)s * Pr / Sg);
+    const int a = spec_seg_start(s, Pr, Sg);
     for (int j = 0; j < Rc; ++j) {
         float* dst = ck + ((int64_t)q * Pr + a + j) * Pd;
         const float* src = ckc + (((int64_t)q * (Sg - 1) + s - 1) * Rc + j) * Pd;

@@ -219,3 +219,29 @@ def test_nested_recomputation_levels_are_exact():
         assert np.array_equal(cc.cpu().numpy().view(np.uint32), ref["cost"].view(np.uint32))
         assert np.array_equal(ee.cpu().numpy(), ref["end"])
     assert np.array_equal(s2.cpu().numpy(), ref["start"])
+
+
+def test_spec_two_segments_split_point():
+    """The two-segment plan splits at 16/25 of the rounds (spec_seg_start):
+    queries copying the reference across THAT boundary defeat one-round corrections and are
+    recomputed (so may others: with N = 1,500 rows against a 960-column correction any query's
+    correction can fail -- the auto correction length is 3N columns); a copy straddling the
+    midpoint, random queries; every result exact against the oracle and the sequential schedule."""
+    M, N = 100_000, 1500
+    Y = oracle.znorm(nanopore_reference(M, 64)[None])[0]
+    Pr = -(-M // 960)                               # one-warp rings: 960 columns per round
+    b = (Pr * 16 // 25) * 960                       # the split column
+    mid = (Pr // 2) * 960
+    Q0, _ = _inputs(3, N, M, 64)
+    Q = np.concatenate([np.stack([Y[b - 200:b + N - 200], Y[mid - 200:mid + N - 200]]), Q0]).astype(np.float32)
+    c, e, fixed, _ = _run(Q, Y, OPT_SCHED=3, OPT_LANES=1, OPT_SPEC_ROUNDS=1, OPT_SEGMENTS=2)
+    assert fixed >= 1
+    _check(Q, Y, c, e)
+    assert c[0] == 0 and e[0] == b + N - 201 and c[1] == 0 and e[1] == mid + N - 201
+    _, _, fixed2, _ = _run(Q[:1], Y, OPT_SCHED=3, OPT_LANES=1, OPT_SPEC_ROUNDS=1, OPT_SEGMENTS=2)
+    assert fixed2 == 1                              # the copy across the split defeats its correction
+    cs, es, _, _ = _run(Q, Y, OPT_SCHED=2, OPT_LANES=1, OPT_SEGMENTS=2)
+    assert np.array_equal(c.view(np.uint32), cs.view(np.uint32)) and np.array_equal(e, es)
+    c, e, fixed, _, st = _run(Q, Y, start=True, OPT_SCHED=3, OPT_LANES=1, OPT_SPEC_ROUNDS=1, OPT_SEGMENTS=2)
+    assert fixed >= 1 and st[0] == b - 200 and st[1] == mid - 200
+    _check(Q, Y, c, e, s=st)

@@ -133,3 +133,22 @@ def test_forced_ckpt_rejects_unqualified_launches():
     assert ei.value.status == sd.E_ARG
     c, e, s, _ = _tb(Q, Y, OPT_START=0, OPT_PACKED=0)      # auto falls back to forward propagation
     _check(Q, Y, c, e, s)
+
+
+def test_ckpt_start_two_segments():
+    """Checkpointed start with the two-segment plan (first segment 16/25 of the rounds): the
+    merge of the correction checkpoints uses the same split (spec_seg_start), both when the
+    correction is overtaken (random queries, a copy straddling the midpoint) and when it fails
+    (a copy straddling the split, recomputed)."""
+    M = 200_000
+    Y = oracle.znorm(nanopore_reference(M, 87)[None])[0]
+    Q0, _ = _inputs(4, 1500, M, 87)
+    cpr = 960
+    Pr = -(-M // cpr)
+    b = (Pr * 16 // 25) * cpr
+    mid = (Pr // 2) * cpr
+    Q = np.concatenate([np.stack([Y[b - 200:b + 1300], Y[mid - 200:mid + 1300]]), Q0]).astype(np.float32)
+    c, e, s, fixed = _tb(Q, Y, OPT_START=2, OPT_SCHED=3, OPT_LANES=1, OPT_SPEC_ROUNDS=1, OPT_SEGMENTS=2)
+    assert fixed >= 1
+    assert c[0] == 0 and s[0] == b - 200 and c[1] == 0 and s[1] == mid - 200
+    _check(Q, Y, c, e, s)
