@@ -832,7 +832,6 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     constexpr int XC = XS ? 1 : xrow_floats(C);
     constexpr int NC = XS ? 1 : xrow_classes(C);
     int* unit_sh = pp + 64;                                     // broadcast of the grabbed unit
-    long long* log_slot = nullptr;                              // diagnostics (P.unit_log), thread 0
     for (int unit_iter = 0;; ++unit_iter) {
     // ---- which unit: (query q, rounds [pa, pb))
     int q, seg = 0, pa = 0, pb = P.Pr;
@@ -844,7 +843,8 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
         if (threadIdx.x == 0) {
             const int raw = atomicAdd(P.counter, 1);
             *unit_sh = (P.order && raw < P.Z * P.S) ? P.order[raw] : raw;
-            log_slot = (P.unit_log && raw < P.Z * P.S) ? P.unit_log + 4L * raw : nullptr;
+            unit_sh[1] = raw;                                   // (diagnostics: re-read at the unit's end)
+            long long* log_slot = (P.unit_log && raw < P.Z * P.S) ? P.unit_log + 4L * raw : nullptr;
             if (log_slot) {
                 unsigned sm;
                 asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
@@ -875,7 +875,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
                 if (++n == (1LL << 26)) { printf("sdtw watchdog: unit %d waits segment\n", u); __trap(); }
             }
         }
-        if (log_slot) log_slot[2] = globaltimer_ns();
+        if (P.unit_log && threadIdx.x == 0 && unit_sh[1] < P.Z * P.S) P.unit_log[4L * unit_sh[1] + 2] = globaltimer_ns();
         __syncthreads();
     } else {
         if (unit_iter > 0) break;
@@ -971,26 +971,24 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     int p0 = (b0 < 0) ? -1 : 0;
     int r0 = (b0 < 0) ? b0 + Pd : 0;
 
-    // warp g runs steps [32*C*g, 32*C*g + span_g): its lanes' bands cover [0, Pl*Pd).
-    // Tail skip (P.tail_skip, calls that consume no end column): in the unit's last round a
-    // warp whose strips all lie beyond the reference (the partial last round of the whole
-    // reference: config 2 has 26.04 rounds) would compute only +inf cells, so its bands
-    // stop one round early and its SMSP issue goes to the other resident rings.  Monotone
-    // in g: the skipping warps are a suffix of the ring.
-    auto bands_of = [&](int g) -> int {
-        if (!CKPT && P.tail_skip && Pl > 1 && ((long)(pa + Pl - 1) * V + 32L * C * g) * WC >= (long)P.M)
-            return Mtot_bands - Pd;
-        return Mtot_bands;
-    };
-    auto span_of = [&](int g) { return (32 * C - 1 + bands_of(g) + K - 1) / K * K; };
-    const bool tail_skipped = bands_of(gw) < Mtot_bands;
-    const int span = span_of(gw);
+    // warp g runs steps [32*C*g, 32*C*g + span): its lanes' bands cover [0, Pl*Pd)
+    const int span = (32 * C - 1 + Mtot_bands + K - 1) / K * K;
     const int t_begin = u_min;
     const int t_end = t_begin + span;
     // a predecessor never publishes past its own end: the successor's trailing
     // (idle-band) chunks must not wait for more
-    const int pred_end = gw > 0 ? u_min - 32 * C + span_of(gw - 1) : 0;   // = t_end of warp gw-1
-    const int last_end = 32 * C * (G - 1) + span_of(G - 1);              // = t_end of warp G-1
+    const int pred_end = t_end - 32 * C;                 // = t_end of warp gw-1
+    const int last_end = 32 * C * (G - 1) + span;        // = t_end of warp G-1
+    // Tail skip (P.tail_skip, calls that consume no end column): in the unit's last round a
+    // warp whose strips all lie beyond the reference (the partial last round of the whole
+    // reference: config 2 has 26.04 rounds) would compute only +inf cells; it stops once its
+    // bands of the earlier rounds are done (t_stop) and then publishes its nominal end, so
+    // every neighbour's wait is unchanged.  Monotone in g: the skipping warps are a suffix.
+    // The few steps a skipping warp runs into the last round read +inf reference samples (and,
+    // past its predecessor's stop, stale inbox entries): +inf cells, never folded -- no lane
+    // reaches row N-1 of that round before t_stop when N >= 32C + K.
+    const int t_stop = (!CKPT && !TRACE && P.tail_skip && Pl > 1 && N >= 32 * C + K && ((long)(pa + Pl - 1) * V + u_min) * WC >= (long)P.M)
+                           ? t_begin + (32 * C - 1 + Mtot_bands - Pd + K - 1) / K * K : t_end;
     const unsigned FULL = 0xffffffffu;
 
     // Reference strips for the lanes' round transitions are staged in shared memory
@@ -1070,7 +1068,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     reset_xb();
     const int Nm1 = N - 1;
 
-    for (int t0 = t_begin; t0 < t_end; t0 += K) {
+    for (int t0 = t_begin; t0 < t_stop; t0 += K) {
         // ---- chunk-level flow control (all lanes, warp-uniform)
         {
             const int np = gw > 0 ? min(t0 + K - 1, pred_end)
@@ -1290,7 +1288,10 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
     }
     // a tail-skipping warp consumes nothing more: its (non-skipping) predecessor must never
     // wait for ring space again (reset by the next unit's prologue)
-    if (tail_skipped && lane == 0 && gw > 0) st_release_hop(pred_cp, INT_MAX / 2, pred_remote);
+    if (t_stop < t_end) {      // tail skipped: nominal end for the successor (and warp 0), and the
+        if (lane == 31) st_release_hop(succ_pp, t_end, succ_remote);        // predecessor never
+        if (lane == 0 && gw > 0) st_release_hop(pred_cp, INT_MAX / 2, pred_remote);   // waits on us again
+    }
 
     // ---- reduction of (cost, col[, start]) over chains, lanes, warps, cluster CTAs
     float bc = best[0];
@@ -1347,7 +1348,7 @@ __global__ void __launch_bounds__(C == 4 ? 128 : 256, C == 4 ? SDTW_C4_MINB : 2)
             __threadfence();
             if (spec) st_release_gpu(P.seg_done + q * P.S + seg, 1);
             else st_release_gpu(P.seg_done + q, seg + 1);
-            if (log_slot) log_slot[3] = globaltimer_ns();
+            if (P.unit_log && unit_sh[1] < P.Z * P.S) P.unit_log[4L * unit_sh[1] + 3] = globaltimer_ns();
         }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");

@@ -245,6 +245,10 @@ __global__ void __launch_bounds__(256, 2) sdtw_dp2_kernel(const DpParams P) {
     const int t_end = t_begin + span;
     const int pred_end = t_end - 32 * C;
     const int last_end = 32 * C * (G - 1) + span;
+    // tail skip (as in sdtw_dp.cuh): a warp whose strips in the reference's partial last round
+    // all start at or beyond M stops after its earlier bands and publishes its nominal end
+    const int t_stop = (P.tail_skip && Pl > 1 && N >= 32 * C + K && ((long)(pa + Pl - 1) * V_ + u_min) * WC >= (long)P.M)
+                           ? t_begin + (32 * C - 1 + Mtot_bands - Pd + K - 1) / K * K : t_end;
 
     float* ystage = reinterpret_cast<float*>(smem + L.off_stage) + warp * (32 * C * WC);
     int pf_round = 0;
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(256, 2) sdtw_dp2_kernel(const DpParams P) {
     reset_xb();
     const int Nm1 = N - 1;
 
-    for (int t0 = t_begin; t0 < t_end; t0 += K) {
+    for (int t0 = t_begin; t0 < t_stop; t0 += K) {
         {
             const int np = gw > 0 ? min(t0 + K - 1, pred_end)
                                   : (t0 + K - 1 >= Pd ? min(t0 + K - Pd + u_last, last_end) : INT_MIN);
@@ -394,6 +398,10 @@ __global__ void __launch_bounds__(256, 2) sdtw_dp2_kernel(const DpParams P) {
         __syncwarp();
         if (lane == 31) st_release_cta(succ_pp, t0 + K);
         if (lane == 0 && gw > 0) st_release_cta(pred_cp, t0 + K);
+    }
+    if (t_stop < t_end) {      // tail skipped: nominal end for the successor, no more waits for ring space
+        if (lane == 31) st_release_cta(succ_pp, t_end);
+        if (lane == 0 && gw > 0) st_release_cta(pred_cp, INT_MAX / 2);
     }
 
     // (cost, col) over chains, lanes, warps

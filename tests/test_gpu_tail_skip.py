@@ -55,3 +55,38 @@ def test_tail_skip_matches_oracle_and_no_skip(fill, sched):
     for k in np.nonzero(e != ref["end"])[0]:
         assert ref["last_rows"][k, e[k]] == ref["cost"][k], (k, e[k], ref["end"][k])
     assert c[0] == 0.0 and e[0] == M - 1
+
+
+def _batch_kind(kind, Q, Y, skip):
+    if skip:
+        os.environ.pop("SDTW_NO_TAIL_SKIP", None)
+    else:
+        os.environ["SDTW_NO_TAIL_SKIP"] = "1"
+    try:
+        opts = dict(OPT_NORMALIZE=0, OPT_PRECISION=16) if kind == "half" else dict(OPT_NORMALIZE=0)
+        with sd.options(**opts):
+            sd.set_reference(torch.as_tensor(Y, device=DEV))
+            Qt = torch.as_tensor(np.ascontiguousarray(Q), device=DEV)
+            c, e = sd.batch_q8(Qt) if kind == "q8" else sd.batch(Qt)
+            torch.cuda.synchronize()
+    finally:
+        os.environ.pop("SDTW_NO_TAIL_SKIP", None)
+    return c.cpu().numpy(), e.cpu().numpy()
+
+
+@pytest.mark.parametrize("kind", ["half", "q8"])
+def test_tail_skip_reduced_precision_kernels(kind):
+    """The packed-half and uint8-codebook kernels (sdtw_dp2.cuh) skip the same way: over
+    reference lengths that leave their last round filled to different depths, the results are
+    bit-identical to the run without the skip, and the verbatim copy of the reference's last
+    N samples is found at cost 0, end M-1; parity against the reduced-precision oracles is
+    in test_gpu_half.py / test_gpu_q8.py."""
+    N, Z = 200, 4
+    for M in range(30_000, 30_000 + 6 * 1_283, 1_283):
+        Y = oracle.znorm(nanopore_reference(M, 73)[None])[0]
+        Q = oracle.znorm(nanopore_queries(Z, N, M, 73))
+        Q[0] = Y[M - N:]
+        c, e = _batch_kind(kind, Q, Y, True)
+        c0, e0 = _batch_kind(kind, Q, Y, False)
+        assert np.array_equal(c.view(np.uint32), c0.view(np.uint32)) and np.array_equal(e, e0), M
+        assert c[0] == 0.0 and e[0] == M - 1, (M, c[0], e[0])
