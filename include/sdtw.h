@@ -81,7 +81,7 @@ enum {
                                give the same start (reading G6) */
     SDTW_OPT_SPEC_ROUNDS = 16, /* speculative segments: rounds of each correction pass (the
                                columns over which the boundary's paths must be overtaken by
-                               the segment's own); 0 = auto (>= 3 query lengths).  A segment
+                               the segment's own); 0 = auto (one query length of columns plus half a round, rounded up to rounds).  A segment
                                whose correction is not overtaken in time is recomputed, so
                                any value gives exact results; it only moves work */
     SDTW_OPT_PRECISION = 14,/* 32 (default): fp32 cells, bit-exact with the fp32 oracle;

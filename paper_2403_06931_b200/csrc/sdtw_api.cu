@@ -337,7 +337,13 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
     // fill the GPU with sequential segments; every segment then starts at once and a
     // correction pass of Rc rounds per segment boundary restores the exact result.
     const int64_t cols = V * WC;
-    const int Rc = o.spec_rounds > 0 ? o.spec_rounds : (int)std::max<int64_t>(1, (3 * N + cols - 1) / cols);
+    // correction length: the query's length in columns plus half a round, rounded up
+    // (a slope-1 path from the boundary is dominated about N columns later).  Round-2 sweep
+    // (profiles/r02aw_*): config 2 best at 2 rounds, config 5 N = 4,000 at 2 (7.51 vs 7.28
+    // TCUPS with the earlier 3N rule's 4), N = 8,000 at 3 (7.27 vs 6.85 with 7); N <= 1,000: 1.
+    // Any length is exact (failed corrections are recomputed); this only moves work.
+    const int Rc = o.spec_rounds > 0 ? o.spec_rounds
+                                     : (int)std::max<int64_t>(1, (N + cols / 2 + cols - 1) / cols);
     const bool spec_ok = !dual && CL == 1 && Pr >= 4 * (int64_t)(Rc + 1);
     if (sched == 3 && !spec_ok)
         return fail(SDTW_E_ARG, "speculative segments need no clusters, OPT_PACKED <= 2 and >= 4 "

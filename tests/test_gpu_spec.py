@@ -225,7 +225,7 @@ def test_spec_two_segments_split_point():
     """The two-segment plan splits at 16/25 of the rounds (spec_seg_start):
     queries copying the reference across THAT boundary defeat one-round corrections and are
     recomputed (so may others: with N = 1,500 rows against a 960-column correction any query's
-    correction can fail -- the auto correction length is 3N columns); a copy straddling the
+    correction can fail -- the auto correction covers N columns plus half a round); a copy straddling the
     midpoint, random queries; every result exact against the oracle and the sequential schedule."""
     M, N = 100_000, 1500
     Y = oracle.znorm(nanopore_reference(M, 64)[None])[0]
