@@ -240,10 +240,14 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
         return fail(SDTW_E_ARG, "unsupported segment width " + std::to_string(W) + " for this chain layout" +
                                     (C == 4 ? " (28)" : C == 2 ? " (14, 30)" : " (7, 15)"));
     const int64_t units = dual ? (Z + 1) / 2 : Z;
-    // ragged batches with short reads: 8-warp rings (r01 c6 sweep, reads 500..8000 vs 1M:
-    // 4 warps 4.26, 6 4.96, 8 5.58 TCUPS; reads 500..2000: 5.20 -> 5.78; reads 2000..8000
-    // keep 4 warps: 6.87 vs 6.61)
-    int GW = o.lanes > 0 ? o.lanes : ((rg && rg->nmin < 2000 && !half && C == 2) ? 8 : 4);
+    // Warps per ring.  Short fixed-length queries: 2-warp rings (round 2, speculative schedule,
+    // 512 queries vs 1M, profiles/r02az_lanes.jsonl, r02ba_*: N = 500 5.40 -> 6.82 TCUPS, N =
+    // 1,000 6.65 -> 7.48; the ring's fill of V steps per unit weighs less against a short round
+    // period); N >= 1,500 keeps 4 (N = 1,500 7.99 vs 7.65, N = 2,000 8.18 vs 7.28).  Ragged
+    // batches: 4 (the round-1 rule of 8-warp rings for short reads, measured under sequential
+    // segments, lost under the speculative schedule: reads 500..8,000 7.52 -> 7.76 with 4,
+    // 500..2,000 5.16 -> 7.14).
+    int GW = o.lanes > 0 ? o.lanes : ((!rg && !half && C == 2 && N <= 1000) ? 2 : 4);
     int CL = o.cluster > 0 ? o.cluster : 1;
     if (GW < 1 || GW > (dual ? 12 : (C == 4 ? 4 : 8)) || CL < 1 || CL > 16 || (dual && CL != 1))
         return fail(SDTW_E_ARG, "lanes / cluster out of range for this kernel");
