@@ -1,7 +1,8 @@
 """GPU parity of the tail skip: in the partial last round of the reference the
 warps whose strips all lie beyond M stop one round early.  For every fill level of that
 round (1, 2, 3 or 4 warps of the ring still holding columns) and every schedule (one CTA
-per query, sequential persistent segments, speculative segments), cost/end must be what the
+per query, sequential persistent segments, speculative segments, a 2-CTA cluster ring, four
+and one chains per lane), cost/end must be what the
 oracle gives and bit-identical to the run without the skip (SDTW_NO_TAIL_SKIP, read per
 call).  Query 0 is cut verbatim from the last N samples of the reference, so its optimum
 (cost 0) sits in the partial round itself."""
@@ -39,11 +40,13 @@ def _batch(Q, Y, opts, skip):
 
 
 @pytest.mark.parametrize("fill", [1, 961, 1921, 2881, 0])
-@pytest.mark.parametrize("sched", [dict(), dict(OPT_SCHED=2, OPT_SEGMENTS=3), dict(OPT_SCHED=3)])
+@pytest.mark.parametrize("sched", [dict(), dict(OPT_SCHED=2, OPT_SEGMENTS=3), dict(OPT_SCHED=3),
+                                   dict(OPT_CLUSTER=2, OPT_LANES=2), dict(OPT_PACKED=2), dict(OPT_PACKED=0)])
 def test_tail_skip_matches_oracle_and_no_skip(fill, sched):
     N, Z = 200, 6
-    cols = sd.round_columns(N)                      # 3840 with the default 4-warp rings
-    M = cols * 12 + fill                            # last round: `fill` columns (0: full)
+    with sd.options(**sched):
+        cols = sd.round_columns(N)                  # 3840 with the default 4-warp rings
+    M = cols * 12 + (fill if fill <= 1 else fill * cols // 3840)   # last round: `fill` (scaled) columns
     Y = oracle.znorm(nanopore_reference(M, 71)[None])[0]
     Q = oracle.znorm(nanopore_queries(Z, N, M, 71))
     Q[0] = Y[M - N:]                                # exact cut at the very end: cost 0, end M-1
