@@ -307,7 +307,10 @@ sdtw_status plan(const Ctx& ctx, int64_t Z, int64_t N, bool trace, LaunchCfg* cf
         auto ctas = [&](int bytes) { return (int)((228 * 1024) / (bytes + 1024)); };
         for (int rs = RS / 2; rs >= std::max(4 * K, 64); rs /= 2) {
             const sdtw::SmemLayout L2 = layout(rs);
-            if (ctas(L2.bytes) > ctas(L.bytes) && ctas(L.bytes) < 3) { RS = rs; L = L2; }
+            // (2-warp rings: up to the register limit of 8 CTAs -- config 5 N = 1,000: RS 1024 -> 512
+            // takes 7 -> 8 CTAs per SM, 6.88 -> 7.12 TCUPS, profiles/r02bl_*)
+            const bool want = ctas(L.bytes) < 3 || (GW <= 2 && ctas(L.bytes) < 16 / GW);
+            if (ctas(L2.bytes) > ctas(L.bytes) && want) { RS = rs; L = L2; }
         }
     }
     if (L.bytes > 227 * 1024) return fail(SDTW_E_ARG, "query too long for shared memory at this config");
